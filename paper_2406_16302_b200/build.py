@@ -1,0 +1,40 @@
+"""Build the sm_100a C-ABI library librr_b200.so in-tree with nvcc (no JIT cache; the .so travels
+with the repository snapshot to the GPU box)."""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "librr_b200.so")
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("rr_capi.cu", "rr_lbvh.cu", "rr_residual.cu")]
+FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "--extended-lambda",
+         "-shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.h*")) + [os.path.join(HERE, "..", "include", "rr.h")]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if force or _stale():
+        tmp = LIB + ".tmp"
+        cmd = ["nvcc", *FLAGS, "-o", tmp, *SOURCES]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+        if verbose:
+            print(r.stderr)
+        with open(os.path.join(HERE, "csrc", "ptxas_info.txt"), "w") as f:
+            f.write(r.stderr)
+        os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force=True, verbose=True))

@@ -1,0 +1,482 @@
+// rr_device.cuh -- device-side scene layout, Philox, BSDFs, camera and LBVH traversal (sm_100a).
+//
+// Paper: /root/reference/PAPER.md (P:Lnnn).  Readings of unstated details: SURVEY.md 8(c) C1-C12, listed
+// in DESIGN.md.  fp32 throughout; the only shared "data" with any other implementation are the input
+// arrays and the fp32 triangle-selection CDFs built by the host code of this library (rr_capi.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define RR_MAX_INST 8
+#define RR_MAXD 10          // RR_MAX_DEPTH: max path edges
+#define RR_MAXV (RR_MAXD + 1)
+#define RR_PI_F 3.14159265358979323846f
+#define RR_INV_PI_F 0.318309886183790671538f
+#define RR_STACK 64
+#define RR_TMAX 1.0e30f  // every query's tmax is below the 'empty child' sentinel box at 3e38
+
+namespace rr {
+
+// ------------------------------------------------------------------------------------------------
+// float3 helpers
+// ------------------------------------------------------------------------------------------------
+__host__ __device__ __forceinline__ float3 f3(float x, float y, float z) { return make_float3(x, y, z); }
+__host__ __device__ __forceinline__ float3 operator+(float3 a, float3 b) { return f3(a.x + b.x, a.y + b.y, a.z + b.z); }
+__host__ __device__ __forceinline__ float3 operator-(float3 a, float3 b) { return f3(a.x - b.x, a.y - b.y, a.z - b.z); }
+__host__ __device__ __forceinline__ float3 operator*(float3 a, float s) { return f3(a.x * s, a.y * s, a.z * s); }
+__host__ __device__ __forceinline__ float3 operator*(float s, float3 a) { return f3(a.x * s, a.y * s, a.z * s); }
+__host__ __device__ __forceinline__ float3 mul3(float3 a, float3 b) { return f3(a.x * b.x, a.y * b.y, a.z * b.z); }
+__host__ __device__ __forceinline__ float dot3(float3 a, float3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__host__ __device__ __forceinline__ float3 cross3(float3 a, float3 b) {
+  return f3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ float3 norm3(float3 a) { return a * rsqrtf(dot3(a, a)); }
+__device__ __forceinline__ float3 norm3_exact(float3 a) { return a * (1.0f / sqrtf(dot3(a, a))); }
+__device__ __forceinline__ bool eq3(float3 a, float3 b) {
+  return __float_as_uint(a.x) == __float_as_uint(b.x) && __float_as_uint(a.y) == __float_as_uint(b.y) &&
+         __float_as_uint(a.z) == __float_as_uint(b.z);
+}
+__device__ __forceinline__ float comp(float3 v, int k) { return k == 0 ? v.x : (k == 1 ? v.y : v.z); }
+__device__ __forceinline__ float3 xf_point(const float* m, float3 p) {
+  return f3(fmaf(m[0], p.x, fmaf(m[1], p.y, fmaf(m[2], p.z, m[3]))),
+            fmaf(m[4], p.x, fmaf(m[5], p.y, fmaf(m[6], p.z, m[7]))),
+            fmaf(m[8], p.x, fmaf(m[9], p.y, fmaf(m[10], p.z, m[11]))));
+}
+__device__ __forceinline__ float3 xf_vec(const float* m, float3 v) {
+  return f3(fmaf(m[0], v.x, fmaf(m[1], v.y, m[2] * v.z)), fmaf(m[4], v.x, fmaf(m[5], v.y, m[6] * v.z)),
+            fmaf(m[8], v.x, fmaf(m[9], v.y, m[10] * v.z)));
+}
+
+// ------------------------------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. 2011).  Counter: (i lo, i hi, l | side << 8,
+// 2*slot + call), key = seed.  u01(x) = (x >> 8) * 2^-24 (exact in fp32).
+// ------------------------------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+#ifdef __CUDA_ARCH__
+    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+#else
+    uint64_t p0 = (uint64_t)0xD2511F53u * c.x, p1 = (uint64_t)0xCD9E8D57u * c.z;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0, hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+#endif
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+__device__ __forceinline__ float u01f(uint32_t x) { return (float)(x >> 8) * (1.0f / 16777216.0f); }
+
+struct Rng {  // the random numbers of one residual sample (technique l, side, index i)
+  uint32_t i_lo, i_hi, ls, k0, k1;
+  __device__ void dims(uint32_t slot, float d[8]) const {
+    uint2 key = make_uint2(k0, k1);
+    uint4 a = philox4x32_10(make_uint4(i_lo, i_hi, ls, 2u * slot), key);
+    uint4 b = philox4x32_10(make_uint4(i_lo, i_hi, ls, 2u * slot + 1u), key);
+    d[0] = u01f(a.x); d[1] = u01f(a.y); d[2] = u01f(a.z); d[3] = u01f(a.w);
+    d[4] = u01f(b.x); d[5] = u01f(b.y); d[6] = u01f(b.z); d[7] = u01f(b.w);
+  }
+  __device__ void dims_lo(uint32_t slot, float d[4]) const {  // d0..d3 only
+    uint4 a = philox4x32_10(make_uint4(i_lo, i_hi, ls, 2u * slot), make_uint2(k0, k1));
+    d[0] = u01f(a.x); d[1] = u01f(a.y); d[2] = u01f(a.z); d[3] = u01f(a.w);
+  }
+  __device__ void dims_hi(uint32_t slot, float d[4]) const {  // d4..d7 only
+    uint4 b = philox4x32_10(make_uint4(i_lo, i_hi, ls, 2u * slot + 1u), make_uint2(k0, k1));
+    d[0] = u01f(b.x); d[1] = u01f(b.y); d[2] = u01f(b.z); d[3] = u01f(b.w);
+  }
+};
+
+// ------------------------------------------------------------------------------------------------
+// Device scene.  Object flags: bit0 edited (dynamic set), bit1 moved (ghost set), bit2 emitter.
+// BVH2 node = 4 float4 (64 B): (c0.lo.x, c0.hi.x, c0.lo.y, c0.hi.y), (c1 ... same), (c0.lo.z, c0.hi.z,
+// c1.lo.z, c1.hi.z), (child0, child1 as int bits, -, -).  child >= 0: internal node, < 0: leaf ~idx.
+// Leaf triangle = 3 float4 (v0.xyz + global tri id bits, v1, v2) in BLAS space.
+// ------------------------------------------------------------------------------------------------
+enum { OBJ_EDITED = 1u, OBJ_MOVED = 2u, OBJ_EMITTER = 4u };
+
+struct DevInstance {
+  int obj, root, moved, pad;
+  float M[2][12];   // object -> world, state 0 = new (N), 1 = old (O)
+  float Mi[2][12];  // world -> object
+  float lo[2][3], hi[2][3];
+};
+
+struct DevScene {
+  const float4* nodes;
+  const float4* ltris;
+  int static_root;  // -1: no static geometry
+  int n_inst;
+  DevInstance inst[RR_MAX_INST];
+  const float4* tverts;      // [3T] by global triangle id (object space for dynamic objects)
+  const uint32_t* tri_obj;
+  const uint32_t* obj_flags;
+  const int* obj_inst;
+  const uint32_t* obj_mat[2];
+  const float4* mat;         // albedo rgb, alpha
+  const uint32_t* mat_type;
+  const float4* obj_emit;
+  const int* obj_emitter;
+  int n_emit;
+  const int* emit_off;
+  const int* emit_cnt;
+  const float* emit_pL;
+  const uint32_t* emit_tris;
+  const float* emit_cdf;
+  int n_edited;
+  const uint32_t* edited_tris;
+  const float* edited_cdf;
+  float pA_D;
+  int n_moved;
+  const uint32_t* moved_tris;
+  const float* moved_cdf;
+  float pA_G;
+  float3 cam_pos, cf, cr, cu;
+  float tanX, tanY, Aplane;
+  int W, H;
+  float eps, diag, dedup_tol;
+};
+
+// ------------------------------------------------------------------------------------------------
+// BSDFs: two-sided, reflection only; wi points toward the previous vertex.
+// ------------------------------------------------------------------------------------------------
+struct Mat {
+  uint32_t type;
+  float3 albedo;
+  float alpha;
+};
+__device__ __forceinline__ Mat load_mat(const DevScene& S, uint32_t obj, int F) {
+  uint32_t m = __ldg(&S.obj_mat[F][obj]);
+  float4 a = __ldg(&S.mat[m]);
+  Mat r;
+  r.type = __ldg(&S.mat_type[m]);
+  r.albedo = f3(a.x, a.y, a.z);
+  r.alpha = a.w;
+  return r;
+}
+__device__ __forceinline__ void onb(float3 n, float3& b1, float3& b2) {  // Duff et al. 2017
+  float sign = copysignf(1.0f, n.z);
+  float a = -1.0f / (sign + n.z);
+  float b = n.x * n.y * a;
+  b1 = f3(1.0f + sign * n.x * n.x * a, sign * b, -sign * n.x);
+  b2 = f3(b, sign + n.y * n.y * a, -n.y);
+}
+__device__ __forceinline__ float3 to_world(float3 n, float x, float y, float z) {
+  float3 b1, b2;
+  onb(n, b1, b2);
+  return b1 * x + b2 * y + n * z;
+}
+__device__ __forceinline__ float ggx_D(float a, float nh) {
+  float a2 = a * a;
+  float t = nh * nh * (a2 - 1.0f) + 1.0f;
+  return a2 / (RR_PI_F * t * t);
+}
+__device__ __forceinline__ float ggx_G1(float a, float nv) {
+  nv = fabsf(nv);
+  return 2.0f * nv / (nv + sqrtf(a * a + (1.0f - a * a) * nv * nv));
+}
+__device__ __forceinline__ float3 bsdf_eval(const Mat& m, float3 n, float3 wi, float3 wo) {
+  float3 ns = dot3(n, wi) > 0.0f ? n : n * -1.0f;
+  float ci = dot3(ns, wi), co = dot3(ns, wo);
+  if (!(ci > 0.0f) || !(co > 0.0f)) return f3(0.f, 0.f, 0.f);
+  if (m.type == 0) return m.albedo * RR_INV_PI_F;
+  float3 h = norm3_exact(wi + wo);
+  float nh = dot3(ns, h);
+  float D = ggx_D(m.alpha, nh);
+  float G = ggx_G1(m.alpha, ci) * ggx_G1(m.alpha, co);
+  float x = 1.0f - fabsf(dot3(wi, h));
+  float x2 = x * x;
+  float fw = x2 * x2 * x;
+  float3 F = m.albedo + (f3(1.f, 1.f, 1.f) - m.albedo) * fw;
+  return F * (D * G / (4.0f * ci * co));
+}
+__device__ __forceinline__ float bsdf_pdf(const Mat& m, float3 n, float3 wi, float3 wo) {
+  float3 ns = dot3(n, wi) > 0.0f ? n : n * -1.0f;
+  float ci = dot3(ns, wi), co = dot3(ns, wo);
+  if (!(ci > 0.0f) || !(co > 0.0f)) return 0.0f;
+  if (m.type == 0) return co * RR_INV_PI_F;
+  float3 h = norm3_exact(wi + wo);
+  float nh = dot3(ns, h);
+  return ggx_D(m.alpha, nh) * fabsf(nh) / (4.0f * fabsf(dot3(wo, h)));
+}
+__device__ __forceinline__ bool bsdf_sample(const Mat& m, float3 n, float3 wi, float u1, float u2, float3& wo) {
+  float3 ns = dot3(n, wi) > 0.0f ? n : n * -1.0f;
+  if (m.type == 0) {
+    float r = sqrtf(u1), phi = 2.0f * RR_PI_F * u2;
+    float s, c;
+    sincosf(phi, &s, &c);
+    wo = norm3_exact(to_world(ns, r * c, r * s, sqrtf(fmaxf(0.0f, 1.0f - u1))));
+    return true;
+  }
+  float a = m.alpha;
+  float tan2 = a * a * u1 / (1.0f - u1);
+  float ct = 1.0f / sqrtf(1.0f + tan2);
+  float st = sqrtf(fmaxf(0.0f, 1.0f - ct * ct));
+  float s, c;
+  sincosf(2.0f * RR_PI_F * u2, &s, &c);
+  float3 h = norm3_exact(to_world(ns, st * c, st * s, ct));
+  float3 w = h * (2.0f * dot3(wi, h)) - wi;
+  if (!(dot3(w, ns) > 0.0f)) return false;
+  wo = norm3_exact(w);
+  return true;
+}
+__device__ __forceinline__ bool rough_enough(const Mat& m, float alpha_min) { return m.type == 0 || m.alpha >= alpha_min; }
+
+// ------------------------------------------------------------------------------------------------
+// camera (C1): pinhole, A_plane = 4 tanX tanY, W_e = 1/(A cos^4), p(x_E) := 1
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ float3 camera_dir(const DevScene& S, float sx, float sy) {
+  return norm3_exact(S.cf + S.cr * ((2.0f * sx / (float)S.W - 1.0f) * S.tanX) +
+                     S.cu * ((1.0f - 2.0f * sy / (float)S.H) * S.tanY));
+}
+__device__ __forceinline__ int project(const DevScene& S, float3 x) {
+  float3 q = x - S.cam_pos;
+  float c = dot3(q, S.cf);
+  if (!(c > 0.0f)) return -1;
+  float sx = (dot3(q, S.cr) / (c * S.tanX) + 1.0f) * (float)S.W * 0.5f;
+  float sy = (1.0f - dot3(q, S.cu) / (c * S.tanY)) * (float)S.H * 0.5f;
+  float fx = floorf(sx), fy = floorf(sy);
+  if (!(fx >= 0.0f) || !(fy >= 0.0f) || fx >= (float)S.W || fy >= (float)S.H) return -1;
+  return (int)fy * S.W + (int)fx;
+}
+
+// ------------------------------------------------------------------------------------------------
+// ray / triangle (watertight, Woop-Benthin-Wald 2013) and ray / box
+// ------------------------------------------------------------------------------------------------
+struct WRay {
+  float3 o, d, inv;
+  int kx, ky, kz;
+  float Sx, Sy, Sz;
+};
+__device__ __forceinline__ WRay make_wray(float3 o, float3 d) {
+  WRay r;
+  r.o = o;
+  r.d = d;
+  r.inv = f3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
+  float ax = fabsf(d.x), ay = fabsf(d.y), az = fabsf(d.z);
+  int kz = (ax > ay) ? (ax > az ? 0 : 2) : (ay > az ? 1 : 2);
+  int kx = kz == 2 ? 0 : kz + 1;
+  int ky = kx == 2 ? 0 : kx + 1;
+  if (comp(d, kz) < 0.0f) {
+    int t = kx;
+    kx = ky;
+    ky = t;
+  }
+  r.kx = kx; r.ky = ky; r.kz = kz;
+  float dz = comp(d, kz);
+  r.Sx = comp(d, kx) / dz;
+  r.Sy = comp(d, ky) / dz;
+  r.Sz = 1.0f / dz;
+  return r;
+}
+// returns t (> 0) or -1
+__device__ __forceinline__ float tri_hit(const WRay& r, float4 a4, float4 b4, float4 c4) {
+  float3 A = f3(a4.x, a4.y, a4.z) - r.o, B = f3(b4.x, b4.y, b4.z) - r.o, C = f3(c4.x, c4.y, c4.z) - r.o;
+  float Az = comp(A, r.kz), Bz = comp(B, r.kz), Cz = comp(C, r.kz);
+  float Ax = comp(A, r.kx) - r.Sx * Az, Ay = comp(A, r.ky) - r.Sy * Az;
+  float Bx = comp(B, r.kx) - r.Sx * Bz, By = comp(B, r.ky) - r.Sy * Bz;
+  float Cx = comp(C, r.kx) - r.Sx * Cz, Cy = comp(C, r.ky) - r.Sy * Cz;
+  float U = Cx * By - Cy * Bx, V = Ax * Cy - Ay * Cx, W = Bx * Ay - By * Ax;
+  if (U == 0.0f || V == 0.0f || W == 0.0f) {  // fall back to double on edges (watertightness)
+    double CxBy = (double)Cx * By, CyBx = (double)Cy * Bx;
+    U = (float)(CxBy - CyBx);
+    double AxCy = (double)Ax * Cy, AyCx = (double)Ay * Cx;
+    V = (float)(AxCy - AyCx);
+    double BxAy = (double)Bx * Ay, ByAx = (double)By * Ax;
+    W = (float)(BxAy - ByAx);
+  }
+  if ((U < 0.0f || V < 0.0f || W < 0.0f) && (U > 0.0f || V > 0.0f || W > 0.0f)) return -1.0f;
+  float det = U + V + W;
+  if (det == 0.0f) return -1.0f;
+  float T = U * (r.Sz * Az) + V * (r.Sz * Bz) + W * (r.Sz * Cz);
+  return T / det;
+}
+__device__ __forceinline__ void box2(const WRay& r, float4 n0, float4 n1, float4 n2, float tmin, float tmax,
+                                     bool& h0, bool& h1, float& t0, float& t1) {
+  float lx0 = (n0.x - r.o.x) * r.inv.x, hx0 = (n0.y - r.o.x) * r.inv.x;
+  float ly0 = (n0.z - r.o.y) * r.inv.y, hy0 = (n0.w - r.o.y) * r.inv.y;
+  float lz0 = (n2.x - r.o.z) * r.inv.z, hz0 = (n2.y - r.o.z) * r.inv.z;
+  float lx1 = (n1.x - r.o.x) * r.inv.x, hx1 = (n1.y - r.o.x) * r.inv.x;
+  float ly1 = (n1.z - r.o.y) * r.inv.y, hy1 = (n1.w - r.o.y) * r.inv.y;
+  float lz1 = (n2.z - r.o.z) * r.inv.z, hz1 = (n2.w - r.o.z) * r.inv.z;
+  float a0 = fmaxf(fmaxf(fminf(lx0, hx0), fminf(ly0, hy0)), fmaxf(fminf(lz0, hz0), tmin));
+  float b0 = fminf(fminf(fmaxf(lx0, hx0), fmaxf(ly0, hy0)), fminf(fmaxf(lz0, hz0), tmax));
+  float a1 = fmaxf(fmaxf(fminf(lx1, hx1), fminf(ly1, hy1)), fmaxf(fminf(lz1, hz1), tmin));
+  float b1 = fminf(fminf(fmaxf(lx1, hx1), fmaxf(ly1, hy1)), fminf(fmaxf(lz1, hz1), tmax));
+  const float g = 1.0000004f;  // conservative slab test
+  h0 = a0 <= b0 * g;
+  h1 = a1 <= b1 * g;
+  t0 = a0;
+  t1 = a1;
+}
+
+// Generic BVH2 traversal.  leaf(leaf_index, t) is called for every triangle hit with t in
+// (tmin, tmax); it returns the new tmax (return a negative value to terminate).
+template <class Leaf>
+__device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay& r, float tmin, float tmax, Leaf leaf) {
+  int stack[RR_STACK];
+  int sp = 0;
+  int node = root;
+  while (true) {
+    if (node >= 0) {
+      const float4* nd = S.nodes + 4 * node;
+      float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
+      bool h0, h1;
+      float t0, t1;
+      box2(r, n0, n1, n2, tmin, tmax, h0, h1, t0, t1);
+      int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
+      if (h0 && h1) {
+        if (t1 < t0) {
+          int t = c0;
+          c0 = c1;
+          c1 = t;
+        }
+        if (sp < RR_STACK) stack[sp++] = c1;
+        node = c0;
+        continue;
+      } else if (h0) {
+        node = c0;
+        continue;
+      } else if (h1) {
+        node = c1;
+        continue;
+      }
+    } else {
+      int li = ~node;
+      const float4* tp = S.ltris + 3 * li;
+      float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
+      float t = tri_hit(r, a, b, c);
+      if (t > tmin && t < tmax) {
+        tmax = leaf(li, t, tmax);
+        if (tmax < 0.0f) return;
+      }
+    }
+    if (sp == 0) return;
+    node = stack[--sp];
+  }
+}
+
+__device__ __forceinline__ int leaf_tri_id(const DevScene& S, int li) { return __float_as_int(__ldg(S.ltris + 3 * li).w); }
+
+// world AABB of instance k in state F vs ray segment
+__device__ __forceinline__ bool inst_box(const DevInstance& I, int F, float3 o, float3 inv, float tmin, float tmax) {
+  float lx = (I.lo[F][0] - o.x) * inv.x, hx = (I.hi[F][0] - o.x) * inv.x;
+  float ly = (I.lo[F][1] - o.y) * inv.y, hy = (I.hi[F][1] - o.y) * inv.y;
+  float lz = (I.lo[F][2] - o.z) * inv.z, hz = (I.hi[F][2] - o.z) * inv.z;
+  float a = fmaxf(fmaxf(fminf(lx, hx), fminf(ly, hy)), fmaxf(fminf(lz, hz), tmin));
+  float b = fminf(fminf(fmaxf(lx, hx), fmaxf(ly, hy)), fminf(fmaxf(lz, hz), tmax));
+  return a <= b * 1.0000004f;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Queries in View_F = static BLAS + edited objects at M_F (ghosts transparent)
+// ------------------------------------------------------------------------------------------------
+struct Hit {
+  float t;
+  int leaf;   // leaf triangle index (-1: miss)
+  int inst;   // -1 static, else instance index
+};
+struct Cross {  // ghost crossings of one segment: count, sum 1/|cos_G|, sum t^2/|cos_G|, sum (L-t)^2/|cos_G|
+  float n, s0, sa, sb;
+};
+__device__ __forceinline__ Cross cross_zero() { Cross c; c.n = c.s0 = c.sa = c.sb = 0.0f; return c; }
+
+struct QCount {  // per-thread query counters
+  uint32_t closest, shadow, inst;
+};
+
+__device__ __forceinline__ Hit closest_static(const DevScene& S, const WRay& r, float tmin, int excl) {
+  Hit h;
+  h.t = RR_TMAX;
+  h.leaf = -1;
+  h.inst = -1;
+  if (S.static_root < 0) return h;
+  traverse(S, S.static_root, r, tmin, RR_TMAX, [&](int li, float t, float tmax) {
+    if (leaf_tri_id(S, li) == excl) return tmax;
+    h.t = t;
+    h.leaf = li;
+    return t;
+  });
+  return h;
+}
+// closest hit among edited instances placed at M_F, beyond tmin and before h.t (updates h)
+__device__ __forceinline__ void closest_dyn(const DevScene& S, int F, float3 o, float3 d, float tmin, int excl, Hit& h) {
+  float3 inv = f3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
+  for (int k = 0; k < S.n_inst; ++k) {
+    const DevInstance& I = S.inst[k];
+    if (!inst_box(I, F, o, inv, tmin, h.t)) continue;
+    WRay r = make_wray(xf_point(I.Mi[F], o), xf_vec(I.Mi[F], d));
+    traverse(S, I.root, r, tmin, h.t, [&](int li, float t, float tmax) {
+      if (leaf_tri_id(S, li) == excl) return tmax;
+      h.t = t;
+      h.leaf = li;
+      h.inst = k;
+      return t;
+    });
+  }
+}
+
+// ghost crossings in state F: hits of MOVED instances placed at M_Fbar, t in (tmin, tmax); segment
+// length L for the (L - t) sums; hits within dedup_tol of an already counted one count once
+__device__ __forceinline__ Cross crossings(const DevScene& S, int F, float3 o, float3 d, float tmin, float tmax, float L) {
+  Cross c = cross_zero();
+  int Fb = 1 - F;
+  float3 inv = f3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
+  float seen[8];
+  int ns = 0;
+  for (int k = 0; k < S.n_inst; ++k) {
+    const DevInstance& I = S.inst[k];
+    if (!I.moved) continue;
+    if (!inst_box(I, Fb, o, inv, tmin, tmax)) continue;
+    float3 od = xf_vec(I.Mi[Fb], d);
+    WRay r = make_wray(xf_point(I.Mi[Fb], o), od);
+    traverse(S, I.root, r, tmin, tmax, [&](int li, float t, float tm) {
+      for (int q = 0; q < ns; ++q)
+        if (fabsf(seen[q] - t) < S.dedup_tol) return tm;
+      if (ns < 8) seen[ns++] = t;
+      const float4* tp = S.ltris + 3 * li;
+      float4 a = __ldg(tp), b = __ldg(tp + 1), cc = __ldg(tp + 2);
+      float3 nrm = norm3_exact(cross3(f3(b.x - a.x, b.y - a.y, b.z - a.z), f3(cc.x - a.x, cc.y - a.y, cc.z - a.z)));
+      float inv_c = 1.0f / fabsf(dot3(nrm, od));
+      c.n += 1.0f;
+      c.s0 += inv_c;
+      c.sa += t * t * inv_c;
+      c.sb += (L - t) * (L - t) * inv_c;
+      return tm;
+    });
+  }
+  return c;
+}
+
+// any hit of static geometry in (tmin, tmax) excluding two triangle ids
+__device__ __forceinline__ bool occluded_static(const DevScene& S, const WRay& r, float tmin, float tmax, int ea, int eb) {
+  if (S.static_root < 0) return false;
+  bool hit = false;
+  traverse(S, S.static_root, r, tmin, tmax, [&](int li, float t, float tm) {
+    int id = leaf_tri_id(S, li);
+    if (id == ea || id == eb) return tm;
+    hit = true;
+    return -1.0f;
+  });
+  return hit;
+}
+__device__ __forceinline__ bool occluded_dyn(const DevScene& S, int F, float3 o, float3 d, float tmin, float tmax, int ea, int eb) {
+  float3 inv = f3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
+  for (int k = 0; k < S.n_inst; ++k) {
+    const DevInstance& I = S.inst[k];
+    if (!inst_box(I, F, o, inv, tmin, tmax)) continue;
+    WRay r = make_wray(xf_point(I.Mi[F], o), xf_vec(I.Mi[F], d));
+    bool hit = false;
+    traverse(S, I.root, r, tmin, tmax, [&](int li, float t, float tm) {
+      int id = leaf_tri_id(S, li);
+      if (id == ea || id == eb) return tm;
+      hit = true;
+      return -1.0f;
+    });
+    if (hit) return true;
+  }
+  return false;
+}
+
+}  // namespace rr

@@ -1,0 +1,40 @@
+// rr_kernels.h -- kernel argument block and launchers (internal; not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rr.h"
+#include "rr_device.cuh"
+
+namespace rr {
+
+enum {
+  STAT_SAMPLES = 0, STAT_CONNECTIONS, STAT_ACCEPTED, STAT_REJECTED, STAT_UNPAIRED, STAT_MAPPED_ONLY,
+  STAT_RECONNECTED, STAT_CLOSEST, STAT_SHADOW, STAT_INST, STAT_SPLATS, STAT_OFFSCREEN, STAT_ZERO,
+  STAT_REJBY, STAT_COUNT = STAT_REJBY + 6
+};
+
+struct KArgs {
+  int tech, tech_q, side, max_depth;
+  uint32_t mask;
+  int two_way, reconnect, reject_multi;
+  uint64_t seed;
+  float sigma, inv_spp, jacobian_max, alpha_min, dmin;
+  uint64_t n_total;                  // samples of this (technique, side) over all shards
+  uint64_t n_local;                  // local sample slots (shard blocks * 2^16, or the dump range)
+  uint64_t shard_index, shard_count;
+  float* image;                      // H*W*4
+  unsigned long long* stats;         // STAT_COUNT counters
+  int dump;
+  uint64_t i_begin;
+  rr_path_record* recs;
+  unsigned long long* rec_count;
+  uint64_t rec_cap;
+};
+
+void launch_residual(const DevScene& S, const KArgs& A, int grid, cudaStream_t st);
+void launch_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out, cudaStream_t st);
+void launch_trace(const DevScene& S, int F, uint32_t n, const float* rays, float* hits, cudaStream_t st);
+void launch_segment(const DevScene& S, uint32_t n, const float* segs, float* out, cudaStream_t st);
+
+}  // namespace rr

@@ -1,0 +1,214 @@
+// rr_lbvh.cu -- GPU LBVH build (Karras 2012 "Maximizing parallelism in the construction of BVHs,
+// octrees, and k-d trees"): 30-bit Morton codes of triangle centroids, CUB radix sort, binary radix tree
+// from longest common prefixes (duplicate keys broken by index), bottom-up AABB refit with atomic
+// arrival counters, and packing into 64-byte BVH2 nodes.  SAH-free by design (north star).
+// Replaces the paper's Embree BVH.
+#include <cub/cub.cuh>
+
+#include "rr_device.cuh"
+#include "rr_internal.h"
+
+namespace rr {
+
+struct Box {
+  float lo[3], hi[3];
+};
+// boxes written by other threads of the same launch: read through L2 (L1 is not coherent)
+__device__ __forceinline__ Box load_box_cg(const Box* b) {
+  const float* f = (const float*)b;
+  Box r;
+  for (int q = 0; q < 3; ++q) {
+    r.lo[q] = __ldcg(f + q);
+    r.hi[q] = __ldcg(f + 3 + q);
+  }
+  return r;
+}
+
+__global__ void k_centroid_bounds(const float4* __restrict__ tris, int n, float* __restrict__ partial) {
+  __shared__ float s[6][256];
+  float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    float4 a = tris[3 * k], b = tris[3 * k + 1], c = tris[3 * k + 2];
+    float cx = (a.x + b.x + c.x) * (1.0f / 3.0f), cy = (a.y + b.y + c.y) * (1.0f / 3.0f), cz = (a.z + b.z + c.z) * (1.0f / 3.0f);
+    lo[0] = fminf(lo[0], cx); lo[1] = fminf(lo[1], cy); lo[2] = fminf(lo[2], cz);
+    hi[0] = fmaxf(hi[0], cx); hi[1] = fmaxf(hi[1], cy); hi[2] = fmaxf(hi[2], cz);
+  }
+  for (int a = 0; a < 3; ++a) {
+    s[a][threadIdx.x] = lo[a];
+    s[3 + a][threadIdx.x] = hi[a];
+  }
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      for (int a = 0; a < 3; ++a) {
+        s[a][threadIdx.x] = fminf(s[a][threadIdx.x], s[a][threadIdx.x + st]);
+        s[3 + a][threadIdx.x] = fmaxf(s[3 + a][threadIdx.x], s[3 + a][threadIdx.x + st]);
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int a = 0; a < 6; ++a) partial[6 * blockIdx.x + a] = s[a][0];
+}
+
+__device__ __forceinline__ uint32_t expand_bits(uint32_t v) {
+  v = (v * 0x00010001u) & 0xFF0000FFu;
+  v = (v * 0x00000101u) & 0x0F00F00Fu;
+  v = (v * 0x00000011u) & 0xC30C30C3u;
+  v = (v * 0x00000005u) & 0x49249249u;
+  return v;
+}
+
+__global__ void k_morton(const float4* __restrict__ tris, int n, const float* __restrict__ partial, int nblocks,
+                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
+  for (int b = 0; b < nblocks; ++b)
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = fminf(lo[a], partial[6 * b + a]);
+      hi[a] = fmaxf(hi[a], partial[6 * b + 3 + a]);
+    }
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  float4 A = tris[3 * k], B = tris[3 * k + 1], C = tris[3 * k + 2];
+  float c[3] = {(A.x + B.x + C.x) * (1.0f / 3.0f), (A.y + B.y + C.y) * (1.0f / 3.0f), (A.z + B.z + C.z) * (1.0f / 3.0f)};
+  uint32_t q[3];
+  for (int a = 0; a < 3; ++a) {
+    float ext = hi[a] - lo[a];
+    float u = ext > 0.0f ? (c[a] - lo[a]) / ext : 0.5f;
+    q[a] = (uint32_t)fminf(fmaxf(u * 1024.0f, 0.0f), 1023.0f);
+  }
+  keys[k] = (expand_bits(q[0]) << 2) | (expand_bits(q[1]) << 1) | expand_bits(q[2]);
+  vals[k] = (uint32_t)k;
+}
+
+__device__ __forceinline__ int delta(const uint32_t* keys, int n, int i, int j) {
+  if (j < 0 || j >= n) return -1;
+  uint32_t a = keys[i], b = keys[j];
+  if (a == b) return 32 + __clz((uint32_t)i ^ (uint32_t)j);
+  return __clz(a ^ b);
+}
+
+// internal node i of the radix tree: children (encoded: >= 0 internal, < 0 leaf ~k) and parents
+__global__ void k_karras(const uint32_t* __restrict__ keys, int n, int* __restrict__ child, int* __restrict__ parent_int,
+                         int* __restrict__ parent_leaf) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n - 1) return;
+  int d = (delta(keys, n, i, i + 1) - delta(keys, n, i, i - 1)) >= 0 ? 1 : -1;
+  int dmin = delta(keys, n, i, i - d);
+  int lmax = 2;
+  while (delta(keys, n, i, i + lmax * d) > dmin) lmax *= 2;
+  int l = 0;
+  for (int t = lmax / 2; t >= 1; t /= 2)
+    if (delta(keys, n, i, i + (l + t) * d) > dmin) l += t;
+  int j = i + l * d;
+  int dnode = delta(keys, n, i, j);
+  int s = 0;
+  for (int div = 2;; div *= 2) {
+    int t = (l + div - 1) / div;
+    if (delta(keys, n, i, i + (s + t) * d) > dnode) s += t;
+    if (t <= 1) break;
+  }
+  int gamma = i + s * d + min(d, 0);
+  int lo = min(i, j), hi = max(i, j);
+  int left = (lo == gamma) ? ~gamma : gamma;
+  int right = (hi == gamma + 1) ? ~(gamma + 1) : gamma + 1;
+  child[2 * i] = left;
+  child[2 * i + 1] = right;
+  if (left < 0) parent_leaf[~left] = i; else parent_int[left] = i;
+  if (right < 0) parent_leaf[~right] = i; else parent_int[right] = i;
+}
+
+__global__ void k_refit(const float4* __restrict__ tris, const uint32_t* __restrict__ order, int n,
+                        const int* __restrict__ child, const int* __restrict__ parent_int,
+                        const int* __restrict__ parent_leaf, Box* __restrict__ ibox, Box* __restrict__ lbox,
+                        int* __restrict__ counter) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  uint32_t t = order[k];
+  float4 a = tris[3 * t], b = tris[3 * t + 1], c = tris[3 * t + 2];
+  Box bx;
+  bx.lo[0] = fminf(a.x, fminf(b.x, c.x)); bx.hi[0] = fmaxf(a.x, fmaxf(b.x, c.x));
+  bx.lo[1] = fminf(a.y, fminf(b.y, c.y)); bx.hi[1] = fmaxf(a.y, fmaxf(b.y, c.y));
+  bx.lo[2] = fminf(a.z, fminf(b.z, c.z)); bx.hi[2] = fmaxf(a.z, fmaxf(b.z, c.z));
+  lbox[k] = bx;
+  if (n == 1) return;
+  __threadfence();
+  int p = parent_leaf[k];
+  while (p >= 0) {
+    if (atomicAdd(&counter[p], 1) == 0) return;  // first arrival stops; the second one merges
+    __threadfence();
+    int c0 = child[2 * p], c1 = child[2 * p + 1];
+    Box b0 = c0 < 0 ? load_box_cg(lbox + ~c0) : load_box_cg(ibox + c0);
+    Box b1 = c1 < 0 ? load_box_cg(lbox + ~c1) : load_box_cg(ibox + c1);
+    Box m;
+    for (int q = 0; q < 3; ++q) {
+      m.lo[q] = fminf(b0.lo[q], b1.lo[q]);
+      m.hi[q] = fmaxf(b0.hi[q], b1.hi[q]);
+    }
+    ibox[p] = m;
+    __threadfence();
+    p = p == 0 ? -1 : parent_int[p];
+  }
+}
+
+__global__ void k_pack(const float4* __restrict__ tris, const uint32_t* __restrict__ order, int n,
+                       const int* __restrict__ child, const Box* __restrict__ ibox, const Box* __restrict__ lbox,
+                       float4* __restrict__ nodes, float4* __restrict__ ltris, int node_base, int leaf_base) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) {
+    uint32_t t = order[k];
+    ltris[3 * (leaf_base + k)] = tris[3 * t];
+    ltris[3 * (leaf_base + k) + 1] = tris[3 * t + 1];
+    ltris[3 * (leaf_base + k) + 2] = tris[3 * t + 2];
+  }
+  int ninternal = n > 1 ? n - 1 : 1;
+  if (k >= ninternal) return;
+  int c0, c1;
+  Box b0, b1;
+  if (n == 1) {
+    c0 = -1;  // ~0 -> leaf 0
+    b0 = lbox[0];
+    c1 = -1;
+    for (int q = 0; q < 3; ++q) { b1.lo[q] = 3e38f; b1.hi[q] = 3e38f; }  // a point beyond every tmax (<= 1e30): never entered
+  } else {
+    c0 = child[2 * k];
+    c1 = child[2 * k + 1];
+    b0 = c0 < 0 ? lbox[~c0] : ibox[c0];
+    b1 = c1 < 0 ? lbox[~c1] : ibox[c1];
+  }
+  int e0 = c0 < 0 ? ~(leaf_base + ~c0) : node_base + c0;
+  int e1 = c1 < 0 ? ~(leaf_base + ~c1) : node_base + c1;
+  float4* nd = nodes + 4 * (node_base + k);
+  nd[0] = make_float4(b0.lo[0], b0.hi[0], b0.lo[1], b0.hi[1]);
+  nd[1] = make_float4(b1.lo[0], b1.hi[0], b1.lo[1], b1.hi[1]);
+  nd[2] = make_float4(b0.lo[2], b0.hi[2], b1.lo[2], b1.hi[2]);
+  nd[3] = make_float4(__int_as_float(e0), __int_as_float(e1), 0.0f, 0.0f);
+}
+
+// Build one BLAS over n >= 1 triangles (3 float4 each, device).  Writes max(n-1,1) nodes at node_base and n
+// leaf triangles at leaf_base.  Returns the root node index (node_base).
+int build_lbvh(const float4* d_tris, int n, float4* d_nodes, float4* d_ltris, int node_base, int leaf_base,
+               cudaStream_t st) {
+  const int TB = 256;
+  int nb = (n + TB - 1) / TB;
+  int nred = nb < 1024 ? nb : 1024;
+  DevBuf<float> partial(6 * nred);
+  DevBuf<uint32_t> keys(n), vals(n), keys2(n), vals2(n);
+  DevBuf<int> child(2 * (n > 1 ? n - 1 : 1)), pint(n > 1 ? n - 1 : 1), pleaf(n), counter(n > 1 ? n - 1 : 1);
+  DevBuf<Box> ibox(n > 1 ? n - 1 : 1), lbox(n);
+  k_centroid_bounds<<<nred, TB, 0, st>>>(d_tris, n, partial.p);
+  k_morton<<<nb, TB, 0, st>>>(d_tris, n, partial.p, nred, keys.p, vals.p);
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, keys2.p, vals.p, vals2.p, n, 0, 30, st);
+  DevBuf<char> tmp(tmp_bytes);
+  cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, keys2.p, vals.p, vals2.p, n, 0, 30, st);
+  cudaMemsetAsync(counter.p, 0, sizeof(int) * (n > 1 ? n - 1 : 1), st);
+  cudaMemsetAsync(pint.p, 0xff, sizeof(int) * (n > 1 ? n - 1 : 1), st);
+  if (n > 1) k_karras<<<(n - 1 + TB - 1) / TB, TB, 0, st>>>(keys2.p, n, child.p, pint.p, pleaf.p);
+  k_refit<<<nb, TB, 0, st>>>(d_tris, vals2.p, n, child.p, pint.p, pleaf.p, ibox.p, lbox.p, counter.p);
+  k_pack<<<nb, TB, 0, st>>>(d_tris, vals2.p, n, child.p, ibox.p, lbox.p, d_nodes, d_ltris, node_base, leaf_base);
+  cudaStreamSynchronize(st);
+  return node_base;
+}
+
+}  // namespace rr

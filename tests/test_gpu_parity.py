@@ -1,0 +1,289 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north star):
+  * per connection record, each term channel: |g - o| <= 1e-4 max(|g|, |o|) (values < 1e-30 count as 0);
+    status, pix_p and pix_q equal; >= 99.9% of records must match (the rest: hit/miss and pixel flips
+    from fp32 vs fp64 ordering);
+  * image: RMSE(gpu - oracle) <= 1e-3 max |oracle|.
+"""
+import dataclasses
+import math
+import multiprocessing as mp
+
+import numpy as np
+import pytest
+
+from rr_inputs import scenes as S
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-4
+TINY = 1e-30
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _renderer(w):
+    from paper_2406_16302_b200 import Renderer
+    r = Renderer(0)
+    r.upload(w.scene)
+    r.set_edit(w.edits)
+    return r
+
+
+def _oracle(w):
+    from oracle import binding as OB
+    return OB.Oracle(w.scene, w.edits)
+
+
+def _key(r):
+    return (int(r.tech), int(r.side), int(r.i), int(r.key_kind), int(r.key_a), int(r.key_b))
+
+
+def _close(g, o):
+    g = np.where(np.abs(g) < TINY, 0.0, g)
+    o = np.where(np.abs(o) < TINY, 0.0, o)
+    return bool(np.all(np.abs(g - o) <= REL * np.maximum(np.abs(g), np.abs(o))))
+
+
+def compare_records(grecs, orecs):
+    """returns (n_records, n_matching, examples of mismatches)"""
+    G = {_key(r): r for r in grecs}
+    O = {_key(r): r for r in orecs}
+    keys = set(G) | set(O)
+    ok, bad = 0, []
+    for k in keys:
+        g, o = G.get(k), O.get(k)
+        if g is None or o is None:
+            bad.append((k, "missing in " + ("gpu" if g is None else "oracle")))
+            continue
+        same = (g.status == o.status and g.pix_p == o.pix_p and g.pix_q == o.pix_q and
+                _close(np.array(g.term_p, np.float64), np.array(o.term_p)) and
+                _close(np.array(g.term_q, np.float64), np.array(o.term_q)))
+        if same:
+            ok += 1
+        else:
+            bad.append((k, (g.status, o.status, g.pix_p, o.pix_p, g.pix_q, o.pix_q, list(g.term_p), list(o.term_p),
+                            list(g.term_q), list(o.term_q), g.R, o.R)))
+    return len(keys), ok, bad
+
+
+def record_parity(w, args, n_per=None, min_frac=0.999, techniques=None):
+    r = _renderer(w)
+    o = _oracle(w)
+    mask = o.effective_mask(args.technique_mask)
+    n = o.sample_range(args) if n_per is None else min(n_per, o.sample_range(args))
+    sides = (0, 1) if (args.flags & 1) else (0,)
+    total = good = 0
+    allbad = []
+    for l in range(1, 8):
+        if not (mask >> (l - 1)) & 1 or (techniques and l not in techniques):
+            continue
+        for s in sides:
+            g = r.dump_paths(args, l, s, 0, n)
+            _, orc, _ = o.residual(args, l, s, 0, n, records=True)
+            t, k, bad = compare_records(g, orc)
+            total += t
+            good += k
+            allbad += bad
+    assert total > 0
+    frac = good / total
+    assert frac >= min_frac, (frac, total, allbad[:10])
+    return frac, total
+
+
+# ---------------------------------------------------------------- building blocks
+def test_philox_bit_exact(torch_cuda):
+    torch = torch_cuda
+    from oracle import binding as OB
+    w = S.config1(8, 8)
+    r = _renderer(w)
+    rng = np.random.default_rng(0)
+    ctr = rng.integers(0, 2 ** 32, size=(4096, 4), dtype=np.uint64).astype(np.uint32)
+    out = r.philox(torch.from_numpy(ctr.view(np.int32)).cuda(), 0x12345678, 0x9abcdef0).cpu().numpy().view(np.uint32)
+    for k in range(0, 4096, 37):
+        assert list(out[k]) == OB.philox(list(ctr[k]), [0x12345678, 0x9abcdef0])
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_lbvh_closest_hit_matches_oracle(torch_cuda, cfg):
+    torch = torch_cuda
+    w = S.load_config(cfg, width=16, height=16)
+    r = _renderer(w)
+    o = _oracle(w)
+    rng = np.random.default_rng(cfg)
+    n = 3000
+    lo, hi = (np.array([0.02] * 3), np.array([0.98] * 3)) if cfg < 3 else (np.array([0.2, 0.05, 0.2]), np.array([9.8, 2.9, 9.8]))
+    org = rng.uniform(lo, hi, size=(n, 3))
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    rays = np.zeros((n, 8), np.float32)
+    rays[:, 0:3] = org
+    rays[:, 3:6] = d
+    rays[:, 6] = np.array([-1] * n, np.int32).view(np.float32)
+    for F in (0, 1):
+        hits = r.trace(F, torch.from_numpy(rays).cuda()).cpu().numpy()
+        agree = 0
+        for k in range(n):
+            ref = o.closest(F, rays[k, 0:3].astype(np.float64), rays[k, 3:6].astype(np.float64))
+            gt = hits[k, 0]
+            if ref[0] < 0:
+                agree += gt < 0
+                continue
+            tri = hits[k, 1:2].view(np.int32)[0]
+            agree += (gt >= 0 and tri == int(ref[1]) and abs(gt - ref[0]) <= 1e-4 * ref[0] + 1e-6)
+        assert agree >= 0.999 * n, (F, agree, n)
+
+
+def test_ghost_crossings_match_oracle(torch_cuda):
+    torch = torch_cuda
+    w = S.config1(16, 16)
+    r = _renderer(w)
+    o = _oracle(w)
+    rng = np.random.default_rng(3)
+    n = 2000
+    segs = np.zeros((n, 6), np.float32)
+    c = S.CUBE_CENTER + S.CUBE_MOVE * 0.5
+    segs[:, 0:3] = c + rng.normal(size=(n, 3)) * 0.3
+    segs[:, 3:6] = c + rng.normal(size=(n, 3)) * 0.3
+    out = r.segment(torch.from_numpy(segs).cuda()).cpu().numpy()
+    agree = 0
+    for k in range(n):
+        a, b = segs[k, 0:3].astype(np.float64), segs[k, 3:6].astype(np.float64)
+        ok = True
+        for F in (0, 1):
+            cr = o.crossings(F, a, b)
+            ok &= int(round(out[k, 5 * F + 1])) == len(cr)
+            if len(cr):
+                s0 = sum(1.0 / abs(np.dot(cc[4:7], (b - a) / np.linalg.norm(b - a))) for cc in cr)
+                ok &= abs(out[k, 5 * F + 2] - s0) <= 1e-3 * s0
+            ok &= bool(out[k, 5 * F] > 0.5) == o.visible(F, a, b)
+        agree += ok
+    assert agree >= 0.999 * n, agree
+
+
+# ---------------------------------------------------------------- per-record parity (C10)
+@pytest.mark.parametrize("flags", [S.PAPER_FLAGS, S.TWO_WAY, 0])
+def test_records_config1_full(torch_cuda, flags):
+    w = S.config1()  # 64x64, 4 spp, D = 4: the full range of every (technique, side)
+    args = dataclasses.replace(w.args, flags=flags)
+    record_parity(w, args)
+
+
+def test_records_config1_deep(torch_cuda):
+    w = S.config1(32, 32, spp=4, max_depth=8)
+    record_parity(w, w.args)
+
+
+def test_records_config2_material_edit(torch_cuda):
+    w = S.config2()  # 256x256, 16 spp, D = 6 (GGX alpha 0.5 -> 0.1 and Lambert 0.8 -> 0.3)
+    record_parity(w, w.args, n_per=40000)
+
+
+def test_records_occluder_reveal(torch_cuda):
+    w = S.occluder_reveal(32, 32, spp=8, max_depth=5)
+    record_parity(w, w.args)
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_records_full_size_configs_sampled(torch_cuda, cfg):
+    """Full BASELINE sizes (scene, camera, resolution, D) -- the first indices of every (technique,
+    side), computed one by one by the oracle."""
+    w = S.load_config(cfg)
+    record_parity(w, w.args, n_per=3000)
+
+
+# ---------------------------------------------------------------- images and exact special cases
+def _oracle_image(a):
+    cfg, W, spp, D, seed, t0, t1 = a
+    from oracle import binding as OB
+    w = S.load_config(cfg, width=W, height=W, spp=spp, max_depth=D)
+    args = dataclasses.replace(w.args, seed=seed)
+    o = OB.Oracle(w.scene, w.edits)
+    img = np.zeros((W, W, 3))
+    n = o.sample_range(args)
+    mask = o.effective_mask(args.technique_mask)
+    for l in range(1, 8):
+        if (mask >> (l - 1)) & 1:
+            for s in (0, 1):
+                o.residual(args, l, s, n * t0 // 8, n * t1 // 8, image=img)
+    return img
+
+
+def test_image_rmse_config1(torch_cuda):
+    torch = torch_cuda
+    W, spp, D, seed = 32, 64, 4, 11
+    w = S.config1(W, W, spp=spp, max_depth=D, seed=seed)
+    r = _renderer(w)
+    img = r.render_residual(w.args)
+    torch.cuda.synchronize()
+    g = img[..., :3].double().cpu().numpy()
+    with mp.get_context("fork").Pool(8) as p:
+        parts = p.map(_oracle_image, [(1, W, spp, D, seed, k, k + 1) for k in range(8)])
+    ref = sum(parts)
+    rmse = math.sqrt(((g - ref) ** 2).mean())
+    assert rmse <= 1e-3 * np.abs(ref).max(), (rmse, np.abs(ref).max())
+
+
+def test_identity_edit_exact_zero_gpu(torch_cuda):
+    torch = torch_cuda
+    w = S.cornell_identity(64, 64, spp=8, max_depth=6)
+    r = _renderer(w)
+    for flags in (S.PAPER_FLAGS, S.TWO_WAY, 0):
+        img = r.render_residual(dataclasses.replace(w.args, flags=flags))
+        torch.cuda.synchronize()
+        assert int(torch.count_nonzero(img)) == 0
+        st = r.get_stats()
+        assert st["samples"] > 0 and st["connections"] > 0
+
+
+def test_albedo_scale_gpu(torch_cuda):
+    k = 0.5
+    w = S.cornell_albedo_scale(k, 32, 32, spp=8)
+    r = _renderer(w)
+    recs = []
+    for l in (1, 7):
+        for s in (0, 1):
+            recs += r.dump_paths(w.args, l, s, 0, 32 * 32 * 4)
+    n = 0
+    for rec in recs:
+        assert rec.status == 0
+        tp, tq = np.array(rec.term_p, np.float64), np.array(rec.term_q, np.float64)
+        tn, to = (tp, tq) if rec.side == 0 else (tq, tp)
+        if np.all(tn == -to):
+            continue
+        np.testing.assert_allclose(tn, -k * to, rtol=2e-6)
+        n += 1
+    assert n > 100
+
+
+def test_sharding_sums_to_unsharded(torch_cuda):
+    torch = torch_cuda
+    w = S.config1(64, 64, spp=64)  # 131072 samples per (technique, side) -> 2 blocks of 2^16
+    r = _renderer(w)
+    full = r.render_residual(w.args).clone()
+    acc = torch.zeros_like(full)
+    for k in range(3):
+        acc += r.render_residual(w.args, shard_index=k, shard_count=3)
+    torch.cuda.synchronize()
+    scale = float(full.abs().max())
+    assert float((acc - full).abs().max()) <= 1e-5 * scale
+
+
+def test_invalid_arguments_are_refused(torch_cuda):
+    from paper_2406_16302_b200 import RRError
+    w = S.config1(16, 16)
+    r = _renderer(w)
+    for bad in (dict(technique_mask=0x3F), dict(spp=3), dict(max_depth=0), dict(max_depth=11),
+                dict(flags=S.RECONNECT)):
+        with pytest.raises(RRError):
+            r.render_residual(dataclasses.replace(w.args, **bad))
+    e = dataclasses.replace(w.edits[0], new_xform=w.edits[0].new_xform * 1.5)
+    with pytest.raises(RRError):
+        r.set_edit([e])
