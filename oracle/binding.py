@@ -113,6 +113,7 @@ def lib():
         L.orc_set_area.restype = C.c_double
         L.orc_set_area.argtypes = [P, C.c_int]
         L.orc_project.argtypes = [P, D]
+        L.orc_debug_sample.argtypes = [P, C.POINTER(Args), C.c_int, C.c_int, C.c_uint64]
     return _lib
 
 
@@ -262,6 +263,10 @@ class Oracle:
         i1 = self.npix * spp if i1 is None else i1
         lib().orc_primal(self.h, F, seed, max_depth, i0, i1, dptr(img), C.byref(st))
         return img / spp, st.as_dict()
+
+    def debug_sample(self, args, tech, side, i):
+        a = self.make_args(args)
+        lib().orc_debug_sample(self.h, C.byref(a), tech, side, i)
 
     # ---- unit-test helpers
     def closest(self, F, o, d, excl=-1):

@@ -483,7 +483,11 @@ struct Vtx {
   int tri = -1, obj = -1;
   int kind = K_SURF;
 };
-inline bool same_vtx(const Vtx& a, const Vtx& b) {
+// Two vertices of the base and mapped paths coincide iff they are the same primitive of the same hit
+// instance at the same point.  A vertex on a MOVED object lies on a different instance in each state
+// (dyn at M_F vs dyn at M_Fbar), so it never coincides (SURVEY 8(c) C7 "hit divergence").
+bool same_vtx_moved(const std::vector<int>& moved, const Vtx& a, const Vtx& b) {
+  if (a.obj >= 0 && moved[a.obj]) return false;
   return a.tri == b.tri && a.kind == b.kind && same(a.p, b.p) && same(a.n, b.n);
 }
 Vtx vtx_of_hit(V3 o, V3 d, const Hit& h) {
@@ -1147,7 +1151,7 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
     for (int m = 1; m <= std::min(nA, nB); ++m) {
       const Vtx& a = gp.A.v[m];
       const Vtx& b = gq.A.v[m];
-      if (!same_vtx(a, b)) div = true;
+      if (!same_vtx_moved(S.moved, a, b)) div = true;
       bool a_ok = m < (int)gp.A.wo_ok.size() && gp.A.wo_ok[m];
       bool b_ok = m < (int)gq.A.wo_ok.size() && gq.A.wo_ok[m];
       bool dir_div = (a_ok != b_ok) || (a_ok && b_ok && !same(gp.A.wo[m], gq.A.wo[m]));
@@ -1207,7 +1211,7 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
   auto same_path = [&](const Path& a, const Path& b) {
     if (a.x.size() != b.x.size()) return false;
     for (size_t m = 0; m < a.x.size(); ++m)
-      if (!same_vtx(a.x[m], b.x[m])) return false;
+      if (!same_vtx_moved(S.moved, a.x[m], b.x[m])) return false;
     return true;
   };
 
@@ -1641,6 +1645,29 @@ int orc_primal(void* h, int F, uint64_t seed, int D, uint64_t i0, uint64_t i1, d
     stats->shadow_rays += cx.C.shadow;
   }
   return 0;
+}
+
+// debug: print the base / mapped connection paths of one sample
+void orc_debug_sample(void* h, const orc_args* A, int tech, int side, uint64_t i) {
+  Oracle* O = (Oracle*)h;
+  Ctx cx;
+  cx.S = &O->S;
+  cx.mask = effective_mask(O->S, A->technique_mask);
+  Stream st{A->seed, i, (uint32_t)tech, (uint32_t)side};
+  int lq = paired_tech(O->S, cx.mask, tech);
+  for (int which = 0; which < 2; ++which) {
+    int F = which == 0 ? side : 1 - side;
+    Gen g = generate(cx, which == 0 ? tech : lq, F, st, (int)A->max_depth);
+    std::printf("%s tech %d state %d ok %d start (%g %g %g) tri %d\n", which == 0 ? "BASE" : "MAPPED",
+                which == 0 ? tech : lq, F, (int)g.ok, g.start.p.x, g.start.p.y, g.start.p.z, g.start.tri);
+    std::vector<Conn> cs = connections(cx, g, st, (int)A->max_depth);
+    for (const Conn& c : cs) {
+      std::printf("  key %d %d %d :", c.key.kind, c.key.a, c.key.b);
+      for (const Vtx& v : c.path.x) std::printf(" [%d o%d e%d (%.5f %.5f %.5f)]", v.tri, v.obj, v.obj >= 0 ? O->S.edited[v.obj] : -1, v.p.x, v.p.y, v.p.z);
+      std::printf("\n");
+    }
+  }
+  std::fflush(stdout);
 }
 
 // ---------------------------------------- unit-test exports ----------------------------------------

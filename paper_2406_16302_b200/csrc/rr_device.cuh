@@ -167,9 +167,13 @@ __device__ __forceinline__ float3 to_world(float3 n, float x, float y, float z) 
   onb(n, b1, b2);
   return b1 * x + b2 * y + n * z;
 }
-__device__ __forceinline__ float ggx_D(float a, float nh) {
+// D(h) = a^2 / (pi ((n.h)^2 (a^2 - 1) + 1)^2), with the denominator written as sin^2 + a^2 cos^2 and
+// sin^2 = |n x h|^2 so that sharp lobes (a = 0.1) do not lose fp32 precision to cancellation
+__device__ __forceinline__ float ggx_D(float a, float3 n, float3 h) {
   float a2 = a * a;
-  float t = nh * nh * (a2 - 1.0f) + 1.0f;
+  float nh = dot3(n, h);
+  float3 c = cross3(n, h);
+  float t = dot3(c, c) + a2 * nh * nh;
   return a2 / (RR_PI_F * t * t);
 }
 __device__ __forceinline__ float ggx_G1(float a, float nv) {
@@ -182,8 +186,7 @@ __device__ __forceinline__ float3 bsdf_eval(const Mat& m, float3 n, float3 wi, f
   if (!(ci > 0.0f) || !(co > 0.0f)) return f3(0.f, 0.f, 0.f);
   if (m.type == 0) return m.albedo * RR_INV_PI_F;
   float3 h = norm3_exact(wi + wo);
-  float nh = dot3(ns, h);
-  float D = ggx_D(m.alpha, nh);
+  float D = ggx_D(m.alpha, ns, h);
   float G = ggx_G1(m.alpha, ci) * ggx_G1(m.alpha, co);
   float x = 1.0f - fabsf(dot3(wi, h));
   float x2 = x * x;
@@ -197,8 +200,7 @@ __device__ __forceinline__ float bsdf_pdf(const Mat& m, float3 n, float3 wi, flo
   if (!(ci > 0.0f) || !(co > 0.0f)) return 0.0f;
   if (m.type == 0) return co * RR_INV_PI_F;
   float3 h = norm3_exact(wi + wo);
-  float nh = dot3(ns, h);
-  return ggx_D(m.alpha, nh) * fabsf(nh) / (4.0f * fabsf(dot3(wo, h)));
+  return ggx_D(m.alpha, ns, h) * fabsf(dot3(ns, h)) / (4.0f * fabsf(dot3(wo, h)));
 }
 __device__ __forceinline__ bool bsdf_sample(const Mat& m, float3 n, float3 wi, float u1, float u2, float3& wo) {
   float3 ns = dot3(n, wi) > 0.0f ? n : n * -1.0f;

@@ -26,7 +26,12 @@ struct PV {  // path vertex in one state
   int tri, obj;  // tri = -1: camera; obj = -1: camera
 };
 
-__device__ __forceinline__ bool same_pv(const PV& a, const PV& b) {
+// forward declaration of the object flags lookup used below
+__device__ __forceinline__ uint32_t oflags(const DevScene& S, int obj);
+// base and mapped vertices coincide iff same primitive, same point, and not on a MOVED object (a vertex
+// on a moved object lies on a different hit instance in each state)
+__device__ __forceinline__ bool same_pv(const DevScene& S, const PV& a, const PV& b) {
+  if (oflags(S, a.obj) & OBJ_MOVED) return false;
   return a.tri == b.tri && eq3(a.p, b.p) && eq3(a.n, b.n);
 }
 __device__ __forceinline__ PV cam_pv(const DevScene& S) {
@@ -401,7 +406,7 @@ __device__ void sample_single(const DevScene& S, const KArgs& A, uint64_t i, con
   for (int m = 1;; ++m) {
     bool hasP = m <= P.n, hasQ = m <= Q.n;
     if (!hasP && (A.two_way || !hasQ)) break;
-    bool vdiff = hasP && hasQ && !same_pv(P.v[m], Q.v[m]);
+    bool vdiff = hasP && hasQ && !same_pv(S, P.v[m], Q.v[m]);
     hdiv = hdiv || vdiff || (hasP != hasQ);
     if (hasP && edited(S, P.v[m].obj)) dynP++;
     if (hasQ && edited(S, Q.v[m].obj)) dynQ++;
@@ -436,7 +441,7 @@ __device__ void sample_single(const DevScene& S, const KArgs& A, uint64_t i, con
           rng.dims((uint32_t)m, d);
           PV L = sample_emitter(S, d[3], d[4], d[5], d[6]);
           Seg2 sp, sq;
-          bool shared = pc && qc_ && same_pv(P.v[m], Q.v[m]);
+          bool shared = pc && qc_ && same_pv(S, P.v[m], Q.v[m]);
           if (shared) {
             sp = seg2(S, P.v[m].p, L.p, P.v[m].tri, L.tri, true, true, o.qc);
             sq = sp;
@@ -487,7 +492,7 @@ __device__ void sample_single(const DevScene& S, const KArgs& A, uint64_t i, con
       if (pc || (qc_ && !A.two_way)) {
         Seg2 sp, sq;
         int pixp = -1, pixq = -1;
-        bool shared = pc && qc_ && same_pv(P.v[m], Q.v[m]);
+        bool shared = pc && qc_ && same_pv(S, P.v[m], Q.v[m]);
         if (pc) pixp = project(S, P.v[m].p);
         if (qc_) pixq = project(S, Q.v[m].p);
         if (shared) {
@@ -778,7 +783,7 @@ __device__ void sample_bidir(const DevScene& S, const KArgs& A, uint64_t i, cons
   PV x[RR_MAXV + 2];
   Cross ce[RR_MAXV + 2];
   // divergence / dynamic-vertex prefix data per side
-  bool sdiff = P.ok && Q.ok && (l == 3) && !same_pv(P.start, Q.start);
+  bool sdiff = P.ok && Q.ok && (l == 3) && !same_pv(S, P.start, Q.start);
   int nA = P.ok ? P.A.n : 0, nB = P.ok ? P.B.n : 0;
   int mA = Q.ok ? Q.A.n : 0, mB = Q.ok ? Q.B.n : 0;
   int NA = max(nA, mA), NB = max(nB, mB);
@@ -810,11 +815,11 @@ __device__ void sample_bidir(const DevScene& S, const KArgs& A, uint64_t i, cons
           bool dv = sdiff;
           int dp = (l == 3) ? 1 : 0, dq = dp;
           for (int j = (l == 3 ? 1 : 0); j <= t; ++j) {
-            if (!same_pv(P.A.v[j], Q.A.v[j])) dv = true;
+            if (!same_pv(S, P.A.v[j], Q.A.v[j])) dv = true;
             if (j >= 1) { dp += edited(S, P.A.v[j].obj); dq += edited(S, Q.A.v[j].obj); }
           }
           for (int j = 1; j <= s; ++j) {
-            if (!same_pv(P.B.v[j], Q.B.v[j])) dv = true;
+            if (!same_pv(S, P.B.v[j], Q.B.v[j])) dv = true;
             dp += edited(S, P.B.v[j].obj);
             dq += edited(S, Q.B.v[j].obj);
           }

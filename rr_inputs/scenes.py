@@ -350,7 +350,9 @@ def _cornell_room(b: _Builder):
     return gray
 
 
-CUBE_CENTER = np.array([0.3, 0.15, 0.4])
+# the dynamic cube rests 1 mm above the floor: its bottom face is never coplanar with the floor, so
+# ray/triangle ties cannot depend on floating-point rounding (readings)
+CUBE_CENTER = np.array([0.3, 0.151, 0.4])
 CUBE_MOVE = np.array([0.1, 0.0, 0.05])
 
 
@@ -493,7 +495,7 @@ def _large_scene(config: int, extra_dynamic: bool):
         centers_dyn.append(np.array([-2.0, 1.5, -20.0]))
         m2 = b.material(Material(LAMBERT, (0.8, 0.8, 0.8)))
         dyn.append(b.add(*box((-0.25, -0.25, -0.25), (0.25, 0.25, 0.25)), m2, flags=OBJ_DYNAMIC))
-        centers_dyn.append(np.array([2.0, 0.25, -21.0]))
+        centers_dyn.append(np.array([2.0, 0.251, -21.0]))  # 1 mm above the ground (no coplanar faces)
     return b, dyn, centers_dyn
 
 

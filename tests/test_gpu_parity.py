@@ -63,7 +63,11 @@ def compare_records(grecs, orecs):
         if g is None or o is None:
             bad.append((k, "missing in " + ("gpu" if g is None else "oracle")))
             continue
-        same = (g.status == o.status and g.pix_p == o.pix_p and g.pix_q == o.pix_q and
+        gp, gq = np.array(g.term_p, np.float64), np.array(g.term_q, np.float64)
+        # a pixel only matters where its term is nonzero (contribution-free records splat nothing)
+        pix_ok = ((g.pix_p == o.pix_p or not (np.any(np.abs(gp) > TINY) or np.any(np.abs(o.term_p) > TINY))) and
+                  (g.pix_q == o.pix_q or not (np.any(np.abs(gq) > TINY) or np.any(np.abs(o.term_q) > TINY))))
+        same = (g.status == o.status and pix_ok and
                 _close(np.array(g.term_p, np.float64), np.array(o.term_p)) and
                 _close(np.array(g.term_q, np.float64), np.array(o.term_q)))
         if same:
