@@ -1663,7 +1663,7 @@ void orc_debug_sample(void* h, const orc_args* A, int tech, int side, uint64_t i
     std::vector<Conn> cs = connections(cx, g, st, (int)A->max_depth);
     for (const Conn& c : cs) {
       std::printf("  key %d %d %d :", c.key.kind, c.key.a, c.key.b);
-      for (const Vtx& v : c.path.x) std::printf(" [%d o%d e%d (%.5f %.5f %.5f)]", v.tri, v.obj, v.obj >= 0 ? O->S.edited[v.obj] : -1, v.p.x, v.p.y, v.p.z);
+      for (const Vtx& v : c.path.x) std::printf(" [%d o%d e%d (%.17g %.17g %.17g) (%.17g %.17g %.17g)]", v.tri, v.obj, v.obj >= 0 ? O->S.edited[v.obj] : -1, v.p.x, v.p.y, v.p.z, v.n.x, v.n.y, v.n.z);
       std::printf("\n");
     }
   }

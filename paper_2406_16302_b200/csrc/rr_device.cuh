@@ -214,7 +214,7 @@ __device__ __forceinline__ bool bsdf_sample(const Mat& m, float3 n, float3 wi, f
   float a = m.alpha;
   float tan2 = a * a * u1 / (1.0f - u1);
   float ct = 1.0f / sqrtf(1.0f + tan2);
-  float st = sqrtf(fmaxf(0.0f, 1.0f - ct * ct));
+  float st = sqrtf(tan2) * ct;  // sin = tan cos: no cancellation for the small angles of sharp lobes
   float s, c;
   sincosf(2.0f * RR_PI_F * u2, &s, &c);
   float3 h = norm3_exact(to_world(ns, st * c, st * s, ct));

@@ -701,7 +701,7 @@ __device__ void gen_bidir(const DevScene& S, const KArgs& A, int tech, int F, co
     if (S.n_moved == 0 || D < 3) return;
     PV xg = sample_set(S, S.moved_tris, S.moved_cdf, S.n_moved, 1 - F, d0[0], d0[1], d0[2]);
     float z = 1.0f - 2.0f * d0[3];
-    float rr = sqrtf(fmaxf(0.0f, 1.0f - z * z)), s, c;
+    float rr = 2.0f * sqrtf(d0[3] * (1.0f - d0[3])), s, c;  // sqrt(1 - z^2) = 2 sqrt(u (1-u)), no cancellation
     sincosf(2.0f * RR_PI_F * d0[4], &s, &c);
     float3 dir = f3(rr * c, rr * s, z);
     Trace2 ty = trace2(S, xg.p, dir, -1, F == 0, F == 1, qc);
