@@ -122,6 +122,8 @@ typedef struct {
   uint64_t shadow_rays;    /* any-hit (connection) queries traversing the static BLAS */
   uint64_t instance_queries; /* dynamic-instance-only queries (crossings / re-checks), not in Mrays */
   uint64_t splats, offscreen, zero_pairs;
+  uint64_t nodes_visited;  /* BVH2 internal nodes fetched (64 B each), all traversals */
+  uint64_t tris_tested;    /* leaf triangles tested (48 B each), all traversals */
   uint64_t rejected_by[8]; /* by reason: 1 occluded, 2 jacobian, 3 multi, 4 target, 5 suffix-dynamic */
   uint32_t effective_mask; /* technique mask after auto-disable (T4-T6 off without moved objects) */
   uint32_t n_moved;        /* moved objects in the current edit */

@@ -17,7 +17,7 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.h*")) + [os.path.join(HERE, "..", "include", "rr.h")]
+    deps = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.h*")) + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(HERE, "..", "include", "rr.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 

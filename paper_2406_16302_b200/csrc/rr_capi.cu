@@ -38,7 +38,7 @@ struct rr_ctx {
   DevBuf<uint32_t> d_tri_obj, obj_flags, mat_type, obj_mat0, obj_mat1, emit_tris, edited_tris, moved_tris;
   DevBuf<int> d_obj_inst, obj_emitter, emit_off, emit_cnt;
   DevBuf<float> emit_pL, emit_cdf, edited_cdf, moved_cdf;
-  DevBuf<unsigned long long> stats;
+  DevBuf<unsigned long long> stats, work;
   DevScene S;
   uint32_t last_mask = 0;
   int edited_equals_moved = 0;
@@ -111,6 +111,7 @@ rr_status rr_create(int cuda_device, rr_ctx** out) {
   std::memset(&c->S, 0, sizeof(c->S));
   try {
     c->stats.alloc(STAT_COUNT);
+    c->work.alloc(16);
   } catch (...) {
     delete c;
     return RR_E_OOM;
@@ -555,9 +556,10 @@ static KArgs make_kargs(rr_ctx* c, const rr_render_args* a, uint32_t mask, int l
   K.stats = c->stats.p;
   return K;
 }
+// persistent lanes: enough blocks to fill every SM (148 on B200) several times, fewer for tiny launches
 static int grid_for(uint64_t n) {
   uint64_t g = (n + 127) / 128;
-  uint64_t cap = 148ull * 16;
+  uint64_t cap = 148ull * 8;
   return (int)std::max<uint64_t>(1, std::min(g, cap));
 }
 
@@ -579,7 +581,8 @@ rr_status rr_render_residual(rr_ctx* c, const rr_render_args* a, float* d_image,
   size_t img_bytes = (size_t)c->cam.width * c->cam.height * 4 * sizeof(float);
   if (!(a->flags & RR_ACCUMULATE)) cudaMemsetAsync(d_image, 0, img_bytes, st);
   cudaMemsetAsync(c->stats.p, 0, STAT_COUNT * sizeof(unsigned long long), st);
-  int ne = 0;
+  cudaMemsetAsync(c->work.p, 0, 16 * sizeof(unsigned long long), st);
+  int ne = 0, nl = 0;
   cudaEventRecord(c->ev[ne++], st);
   int sides = (a->flags & RR_TWO_WAY) ? 2 : 1;
   for (int l = 1; l <= 7; ++l) {
@@ -587,6 +590,7 @@ rr_status rr_render_residual(rr_ctx* c, const rr_render_args* a, float* d_image,
     for (int side = 0; side < sides; ++side) {
       KArgs K = make_kargs(c, a, mask, l, side);
       K.image = d_image;
+      K.work = c->work.p + (nl++);
       if (K.n_local == 0) continue;
       launch_residual(c->S, K, grid_for(K.n_local), st);
       if (ne < 16) cudaEventRecord(c->ev[ne++], st);
@@ -634,6 +638,8 @@ rr_status rr_get_stats(rr_ctx* c, rr_stats* out) {
   out->splats = h[STAT_SPLATS];
   out->offscreen = h[STAT_OFFSCREEN];
   out->zero_pairs = h[STAT_ZERO];
+  out->nodes_visited = h[STAT_NODES];
+  out->tris_tested = h[STAT_TRIS];
   for (int r = 0; r < 6; ++r) out->rejected_by[r] = h[STAT_REJBY + r];
   out->effective_mask = c->last_mask;
   out->n_moved = 0;
@@ -669,7 +675,9 @@ rr_status rr_dump_paths(rr_ctx* c, const rr_render_args* a, uint32_t technique, 
     DevBuf<float> img(4);
     cudaMemset(cnt.p, 0, sizeof(unsigned long long));
     cudaMemset(c->stats.p, 0, STAT_COUNT * sizeof(unsigned long long));
+    cudaMemset(c->work.p, 0, 16 * sizeof(unsigned long long));
     KArgs K = make_kargs(c, a, mask, (int)technique, (int)side);
+    K.work = c->work.p;
     K.image = img.p;
     K.dump = 1;
     K.i_begin = i_begin;

@@ -315,13 +315,18 @@ __device__ __forceinline__ void box2(const WRay& r, float4 n0, float4 n1, float4
 
 // Generic BVH2 traversal.  leaf(leaf_index, t) is called for every triangle hit with t in
 // (tmin, tmax); it returns the new tmax (return a negative value to terminate).
+struct TCount {  // traversal work of one thread: internal nodes fetched, triangles tested (64 B / 48 B each)
+  uint32_t nodes, tris;
+};
 template <class Leaf>
-__device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay& r, float tmin, float tmax, Leaf leaf) {
+__device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay& r, float tmin, float tmax, Leaf leaf,
+                                         TCount& tc) {
   int stack[RR_STACK];
   int sp = 0;
   int node = root;
   while (true) {
     if (node >= 0) {
+      tc.nodes++;
       const float4* nd = S.nodes + 4 * node;
       float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
       bool h0, h1;
@@ -346,6 +351,7 @@ __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay
       }
     } else {
       int li = ~node;
+      tc.tris++;
       const float4* tp = S.ltris + 3 * li;
       float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
       float t = tri_hit(r, a, b, c);
@@ -386,9 +392,10 @@ __device__ __forceinline__ Cross cross_zero() { Cross c; c.n = c.s0 = c.sa = c.s
 
 struct QCount {  // per-thread query counters
   uint32_t closest, shadow, inst;
+  TCount tc;
 };
 
-__device__ __forceinline__ Hit closest_static(const DevScene& S, const WRay& r, float tmin, int excl) {
+__device__ __forceinline__ Hit closest_static(const DevScene& S, const WRay& r, float tmin, int excl, TCount& tc) {
   Hit h;
   h.t = RR_TMAX;
   h.leaf = -1;
@@ -399,11 +406,12 @@ __device__ __forceinline__ Hit closest_static(const DevScene& S, const WRay& r, 
     h.t = t;
     h.leaf = li;
     return t;
-  });
+  }, tc);
   return h;
 }
 // closest hit among edited instances placed at M_F, beyond tmin and before h.t (updates h)
-__device__ __forceinline__ void closest_dyn(const DevScene& S, int F, float3 o, float3 d, float tmin, int excl, Hit& h) {
+__device__ __forceinline__ void closest_dyn(const DevScene& S, int F, float3 o, float3 d, float tmin, int excl, Hit& h,
+                                            TCount& tc) {
   float3 inv = f3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
   for (int k = 0; k < S.n_inst; ++k) {
     const DevInstance& I = S.inst[k];
@@ -415,13 +423,14 @@ __device__ __forceinline__ void closest_dyn(const DevScene& S, int F, float3 o, 
       h.leaf = li;
       h.inst = k;
       return t;
-    });
+    }, tc);
   }
 }
 
 // ghost crossings in state F: hits of MOVED instances placed at M_Fbar, t in (tmin, tmax); segment
 // length L for the (L - t) sums; hits within dedup_tol of an already counted one count once
-__device__ __forceinline__ Cross crossings(const DevScene& S, int F, float3 o, float3 d, float tmin, float tmax, float L) {
+__device__ __forceinline__ Cross crossings(const DevScene& S, int F, float3 o, float3 d, float tmin, float tmax, float L,
+                                           TCount& tc) {
   Cross c = cross_zero();
   int Fb = 1 - F;
   float3 inv = f3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
@@ -446,13 +455,14 @@ __device__ __forceinline__ Cross crossings(const DevScene& S, int F, float3 o, f
       c.sa += t * t * inv_c;
       c.sb += (L - t) * (L - t) * inv_c;
       return tm;
-    });
+    }, tc);
   }
   return c;
 }
 
 // any hit of static geometry in (tmin, tmax) excluding two triangle ids
-__device__ __forceinline__ bool occluded_static(const DevScene& S, const WRay& r, float tmin, float tmax, int ea, int eb) {
+__device__ __forceinline__ bool occluded_static(const DevScene& S, const WRay& r, float tmin, float tmax, int ea, int eb,
+                                                TCount& tc) {
   if (S.static_root < 0) return false;
   bool hit = false;
   traverse(S, S.static_root, r, tmin, tmax, [&](int li, float t, float tm) {
@@ -460,10 +470,11 @@ __device__ __forceinline__ bool occluded_static(const DevScene& S, const WRay& r
     if (id == ea || id == eb) return tm;
     hit = true;
     return -1.0f;
-  });
+  }, tc);
   return hit;
 }
-__device__ __forceinline__ bool occluded_dyn(const DevScene& S, int F, float3 o, float3 d, float tmin, float tmax, int ea, int eb) {
+__device__ __forceinline__ bool occluded_dyn(const DevScene& S, int F, float3 o, float3 d, float tmin, float tmax, int ea, int eb,
+                                             TCount& tc) {
   float3 inv = f3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
   for (int k = 0; k < S.n_inst; ++k) {
     const DevInstance& I = S.inst[k];
@@ -475,7 +486,7 @@ __device__ __forceinline__ bool occluded_dyn(const DevScene& S, int F, float3 o,
       if (id == ea || id == eb) return tm;
       hit = true;
       return -1.0f;
-    });
+    }, tc);
     if (hit) return true;
   }
   return false;

@@ -11,7 +11,7 @@ namespace rr {
 enum {
   STAT_SAMPLES = 0, STAT_CONNECTIONS, STAT_ACCEPTED, STAT_REJECTED, STAT_UNPAIRED, STAT_MAPPED_ONLY,
   STAT_RECONNECTED, STAT_CLOSEST, STAT_SHADOW, STAT_INST, STAT_SPLATS, STAT_OFFSCREEN, STAT_ZERO,
-  STAT_REJBY, STAT_COUNT = STAT_REJBY + 6
+  STAT_NODES, STAT_TRIS, STAT_REJBY, STAT_COUNT = STAT_REJBY + 6
 };
 
 struct KArgs {
@@ -25,6 +25,7 @@ struct KArgs {
   uint64_t shard_index, shard_count;
   float* image;                      // H*W*4
   unsigned long long* stats;         // STAT_COUNT counters
+  unsigned long long* work;          // sample-slot counter of this launch (zeroed before the launch)
   int dump;
   uint64_t i_begin;
   rr_path_record* recs;

@@ -1,0 +1,169 @@
+// rr_query.cuh -- the one generic ray query of the residual kernels.
+//
+// Every traversal of the estimator goes through run_query(), which contains the kernel's ONLY traversal
+// loop: a query is decomposed into BLAS jobs (the static BLAS once, then each dynamic instance under the
+// transform of each requested state, then each MOVED instance under the other state's transform for the
+// ghost crossings), and one traverse() call site serves every job.  Lanes of a warp that issue queries of
+// different kinds therefore still execute the same instruction stream (SIMT-converged traversal).
+//
+//  QT_CLOSEST: closest hit of the ray (o, d) in View_F = static + dyn at M_F (ghosts transparent),
+//              t in (eps, inf), origin triangle excluded, for each requested state F; plus the ghost
+//              crossings of the resulting edge in (eps, t_F - eps).  The static BLAS is traversed
+//              once for both states.
+//  QT_SEG:     visibility of the segment (o, o + L d) in View_F, t in (eps, L - eps), both endpoint
+//              triangles excluded; plus its ghost crossings per state.  dyn_only skips the static BLAS
+//              (re-check of a shared suffix edge against dyn_Fbar, P:L429 / P:L500).
+#pragma once
+#include "rr_device.cuh"
+
+namespace rr {
+
+enum { QT_CLOSEST = 0, QT_SEG = 1 };
+
+struct Query {
+  float3 o, d;
+  float tmax;            // QT_SEG: segment length L; QT_CLOSEST: unused
+  int ea, eb;            // excluded triangles (origin, end)
+  uint8_t type, want;    // want: bit F set -> evaluate state F
+  uint8_t dyn_only, pad;
+};
+
+struct QRes {
+  Hit h[2];        // QT_CLOSEST: hit per state (leaf < 0: miss)
+  Cross c[2];      // ghost crossings per state
+  uint8_t ok[2];   // QT_CLOSEST: hit found; QT_SEG: visible
+};
+
+__device__ __noinline__ void run_query(const DevScene& S, const Query& q, QRes& r, QCount& qc) {
+  const bool seg = q.type == QT_SEG;
+  const float L = q.tmax;
+  r.ok[0] = r.ok[1] = 0;
+  r.c[0] = r.c[1] = cross_zero();
+  r.h[0].leaf = r.h[1].leaf = -1;
+  r.h[0].inst = r.h[1].inst = -1;
+  if (seg && !(L > 2.0f * S.eps)) return;
+  float best_t[2], thi = seg ? L - S.eps : RR_TMAX;
+  int best_leaf[2] = {-1, -1}, best_inst[2] = {-1, -1};
+  best_t[0] = best_t[1] = thi;
+  bool blocked[2] = {false, false};
+  bool sblock = false;
+  float seen[8];
+  int ns = 0, seen_state = -1;
+  const int NI = S.n_inst;
+  const int njobs = 1 + 4 * NI;
+  for (int j = 0; j < njobs; ++j) {
+    int kind, F = 0, k = -1;
+    if (j == 0) {
+      kind = 0;
+      if (q.dyn_only || S.static_root < 0) continue;
+    } else {
+      int jj = j - 1, grp = jj / NI;
+      k = jj - grp * NI;
+      kind = grp < 2 ? 1 : 2;
+      F = grp & 1;
+      if (!((q.want >> F) & 1)) continue;
+      if (seg && (sblock || blocked[F])) continue;
+      if (kind == 2 && !S.inst[k].moved) continue;
+      if (kind == 2 && !seg && best_leaf[F] < 0) continue;  // escaped ray: no edge, no crossings
+    }
+    int root, place = 0;
+    float tmin = S.eps, tmax;
+    float3 o = q.o, d = q.d;
+    if (kind == 0) {
+      root = S.static_root;
+      tmax = thi;
+      if (seg) qc.shadow++; else qc.closest++;
+    } else {
+      const DevInstance& I = S.inst[k];
+      place = kind == 1 ? F : 1 - F;
+      tmax = kind == 1 ? best_t[F] : (seg ? L - S.eps : best_t[F] - S.eps);
+      float3 inv = f3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
+      if (!inst_box(I, place, o, inv, tmin, tmax)) continue;
+      o = xf_point(I.Mi[place], q.o);
+      d = xf_vec(I.Mi[place], q.d);
+      root = I.root;
+      if (kind == 2) {
+        qc.inst++;
+        if (seen_state != F) {
+          ns = 0;
+          seen_state = F;
+        }
+      }
+    }
+    const float Lc = seg ? L : best_t[F];  // segment length for the (L - t) crossing sums
+    WRay wr = make_wray(o, d);
+    traverse(S, root, wr, tmin, tmax, [&](int li, float t, float tm) -> float {
+      if (kind == 2) {  // ghost crossing (all hits, dedup within dedup_tol)
+        for (int a = 0; a < ns; ++a)
+          if (fabsf(seen[a] - t) < S.dedup_tol) return tm;
+        if (ns < 8) seen[ns++] = t;
+        const float4* tp = S.ltris + 3 * li;
+        float4 a4 = __ldg(tp), b4 = __ldg(tp + 1), c4 = __ldg(tp + 2);
+        float3 nrm = norm3_exact(cross3(f3(b4.x - a4.x, b4.y - a4.y, b4.z - a4.z), f3(c4.x - a4.x, c4.y - a4.y, c4.z - a4.z)));
+        float inv_c = 1.0f / fabsf(dot3(nrm, d));
+        Cross& cc = r.c[F];
+        cc.n += 1.0f;
+        cc.s0 += inv_c;
+        cc.sa += t * t * inv_c;
+        cc.sb += (Lc - t) * (Lc - t) * inv_c;
+        return tm;
+      }
+      int id = leaf_tri_id(S, li);
+      if (id == q.ea || (seg && id == q.eb)) return tm;
+      if (seg) {  // any hit
+        if (kind == 0) sblock = true; else blocked[F] = true;
+        return -1.0f;
+      }
+      if (kind == 0) {
+        best_t[0] = best_t[1] = t;
+        best_leaf[0] = best_leaf[1] = li;
+        best_inst[0] = best_inst[1] = -1;
+      } else {
+        best_t[F] = t;
+        best_leaf[F] = li;
+        best_inst[F] = k;
+      }
+      return t;
+    }, qc.tc);
+  }
+  for (int F = 0; F < 2; ++F) {
+    if (!((q.want >> F) & 1)) continue;
+    if (seg) {
+      r.ok[F] = (!sblock && !blocked[F]) ? 1 : 0;
+    } else {
+      r.ok[F] = best_leaf[F] >= 0 ? 1 : 0;
+      r.h[F].t = best_t[F];
+      r.h[F].leaf = best_leaf[F];
+      r.h[F].inst = best_inst[F];
+    }
+  }
+}
+
+__device__ __forceinline__ Query mk_ray(float3 o, float3 d, int excl, int want) {
+  Query q;
+  q.o = o;
+  q.d = d;
+  q.tmax = RR_TMAX;
+  q.ea = excl;
+  q.eb = -1;
+  q.type = QT_CLOSEST;
+  q.want = (uint8_t)want;
+  q.dyn_only = 0;
+  return q;
+}
+__device__ __forceinline__ Query mk_seg(float3 a, float3 b, int ea, int eb, int want, bool dyn_only = false) {
+  Query q;
+  float3 dv = b - a;
+  float L = sqrtf(dot3(dv, dv));
+  q.o = a;
+  q.d = dv * (1.0f / L);
+  q.tmax = L;
+  q.ea = ea;
+  q.eb = eb;
+  q.type = QT_SEG;
+  q.want = (uint8_t)want;
+  q.dyn_only = dyn_only ? 1 : 0;
+  return q;
+}
+
+}  // namespace rr

@@ -1,685 +1,519 @@
 // rr_residual.cu -- the residual path integral estimator on the GPU (sm_100a).
 //
-// One thread = one residual sample (technique l, side s, index i).  The base path is
-// generated in state F = side, the mapped path in Fbar with the same Philox counters (random-seed replay,
-// P:L414-416) by the paired technique (dynamic<->ghost pair T2<->T5).  The two walks run in
-// lockstep so that the static-BLAS traversal is shared while the walks have not diverged (A3), the
-// reconnection ("keep vertex the same") is decided at the first diverged rough vertex, and
-// connections are evaluated and splatted as soon as they are formed.
+// One residual sample = one technique invocation (technique l, side s, index i).  The
+// base path is generated in state F = side, the mapped path in Fbar with the same Philox counters
+// (random-seed replay) by the paired technique (dynamic<->ghost pair T2<->T5).
 //
-// MIS is evaluated per connection path as ratios to the PT (T7) pdf: every candidate pdf
-// p_c / p_T7 reduces to products of per-edge reverse/forward pdf ratios (the 1/d^2 factors cancel), and
-// ghost crossings enter only through three per-edge sums (count, sum 1/|cos_G|, sum d^2/|cos_G| toward
-// either endpoint), so no per-crossing records are stored (P:L354 realised as running sums).
+// Execution model (B200): persistent lanes, each running a sample as a state machine.  Every step a lane
+// consumes the results of the ray queries it issued in the previous step, advances its sample (shading,
+// MIS, mapping, splat) and issues the next batch of queries (<= NQ).  The queries of all lanes then run
+// through run_query(), the kernel's single traversal site (rr_query.cuh), so divergent samples still
+// traverse in SIMT lockstep.  A lane whose sample finishes refills from a global sample counter
+// (warp-aggregated atomics): finished paths never occupy a lane ("compaction + refill", A9).
+//
+// The two walks of a single-walk sample run in lockstep so that the static-BLAS traversal is shared while
+// they have not diverged (A3), the reconnection ("keep vertex the same") is decided at the first
+// diverged rough vertex, and connections are evaluated and splatted as soon as they are formed.
 #include <cuda_runtime.h>
 
 #include "rr_device.cuh"
 #include "rr_kernels.h"
+#include "rr_query.cuh"
+#include "rr_shade.cuh"
 
 namespace rr {
 
-enum { ST_ACCEPTED = 0, ST_REJECTED = 1, ST_UNPAIRED = 2, ST_MAPPED_ONLY = 3 };
-enum { RJ_NONE = 0, RJ_OCCLUDED = 1, RJ_JACOBIAN = 2, RJ_MULTI = 3, RJ_TARGET = 4, RJ_SUFFIX_DYN = 5 };
+#define NQ 10
+#define FULLMASK 0xffffffffu
 
-struct PV {  // path vertex in one state
-  float3 p, n;
-  int tri, obj;  // tri = -1: camera; obj = -1: camera
+struct Batch {
+  Query q[NQ];
+  QRes r[NQ];
+  int n;
+  __device__ __forceinline__ int push(const Query& x) {
+    q[n] = x;
+    return n++;
+  }
 };
-
-// forward declaration of the object flags lookup used below
-__device__ __forceinline__ uint32_t oflags(const DevScene& S, int obj);
-// base and mapped vertices coincide iff same primitive, same point, and not on a MOVED object (a vertex
-// on a moved object lies on a different hit instance in each state)
-__device__ __forceinline__ bool same_pv(const DevScene& S, const PV& a, const PV& b) {
-  if (oflags(S, a.obj) & OBJ_MOVED) return false;
-  return a.tri == b.tri && eq3(a.p, b.p) && eq3(a.n, b.n);
-}
-__device__ __forceinline__ PV cam_pv(const DevScene& S) {
-  PV v;
-  v.p = S.cam_pos;
-  v.n = S.cf;
-  v.tri = -1;
-  v.obj = -1;
-  return v;
-}
-__device__ __forceinline__ uint32_t oflags(const DevScene& S, int obj) { return obj < 0 ? 0u : __ldg(&S.obj_flags[obj]); }
-__device__ __forceinline__ bool edited(const DevScene& S, int obj) { return (oflags(S, obj) & OBJ_EDITED) != 0u; }
-
-// hit -> vertex in state F
-__device__ __forceinline__ PV hit_pv(const DevScene& S, const Hit& h, float3 o, float3 d, int F) {
-  PV v;
-  v.p = o + d * h.t;
-  const float4* tp = S.ltris + 3 * h.leaf;
-  float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
-  float3 n = cross3(f3(b.x - a.x, b.y - a.y, b.z - a.z), f3(c.x - a.x, c.y - a.y, c.z - a.z));
-  if (h.inst >= 0) n = xf_vec(S.inst[h.inst].M[F], n);
-  v.n = norm3_exact(n);
-  v.tri = __float_as_int(a.w);
-  v.obj = (int)__ldg(&S.tri_obj[v.tri]);
-  return v;
-}
-
-// area-uniform point on a triangle set (C3): first k with cdf[k] > u0; su = sqrt(u1); b0 = 1-su; b1 = u2 su
-__device__ PV sample_set(const DevScene& S, const uint32_t* tris, const float* cdf, int n, int F, float u0, float u1,
-                         float u2) {
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (__ldg(&cdf[mid]) > u0) hi = mid; else lo = mid + 1;
-  }
-  int tri = (int)__ldg(&tris[lo]);
-  float4 a = __ldg(&S.tverts[3 * tri]), b = __ldg(&S.tverts[3 * tri + 1]), c = __ldg(&S.tverts[3 * tri + 2]);
-  float su = sqrtf(u1);
-  float b0 = 1.0f - su, b1 = u2 * su, b2 = 1.0f - b0 - b1;
-  float3 x = f3(a.x, a.y, a.z) * b0 + f3(b.x, b.y, b.z) * b1 + f3(c.x, c.y, c.z) * b2;
-  float3 nrm = cross3(f3(b.x - a.x, b.y - a.y, b.z - a.z), f3(c.x - a.x, c.y - a.y, c.z - a.z));
-  int obj = (int)__ldg(&S.tri_obj[tri]);
-  int k = __ldg(&S.obj_inst[obj]);
-  if (k >= 0) {
-    x = xf_point(S.inst[k].M[F], x);
-    nrm = xf_vec(S.inst[k].M[F], nrm);
-  }
-  PV v;
-  v.p = x;
-  v.n = norm3_exact(nrm);
-  v.tri = tri;
-  v.obj = obj;
-  return v;
-}
-// NEE emitter sample (C3): object min(floor(d3 n_obj), n_obj-1), then area-uniform within it
-__device__ __forceinline__ PV sample_emitter(const DevScene& S, float d3, float d4, float d5, float d6) {
-  int e = min((int)floorf(d3 * (float)S.n_emit), S.n_emit - 1);
-  int off = __ldg(&S.emit_off[e]), cnt = __ldg(&S.emit_cnt[e]);
-  return sample_set(S, S.emit_tris + off, S.emit_cdf + off, cnt, 0, d4, d5, d6);
-}
-
-// ------------------------------------------------------------------------------------------------
-// query helpers (both states at once where the geometry is shared; A3/A3b/A4)
-// ------------------------------------------------------------------------------------------------
-struct Trace2 {
-  bool ok[2];
-  PV v[2];
-  Cross c[2];
-};
-// closest hit from o along d in View_F for each requested state, with the ghost crossings of the
-// resulting edge (eps, t_F - eps).  The static BLAS is traversed once.
-__device__ Trace2 trace2(const DevScene& S, float3 o, float3 d, int excl, bool want0, bool want1, QCount& qc) {
-  Trace2 r;
-  r.ok[0] = r.ok[1] = false;
-  WRay wr = make_wray(o, d);
-  Hit hs = closest_static(S, wr, S.eps, excl);
-  qc.closest++;
-  for (int F = 0; F < 2; ++F) {
-    if (!(F == 0 ? want0 : want1)) continue;
-    Hit h = hs;
-    closest_dyn(S, F, o, d, S.eps, excl, h);
-    if (h.leaf < 0) continue;
-    r.ok[F] = true;
-    r.v[F] = hit_pv(S, h, o, d, F);
-    r.c[F] = S.n_moved > 0 ? crossings(S, F, o, d, S.eps, h.t - S.eps, h.t) : cross_zero();
-    if (S.n_moved > 0) qc.inst++;
-  }
-  return r;
-}
-struct Seg2 {
-  bool vis[2];
-  Cross c[2];
-};
-// segment a -> b: visibility in View_F (both endpoint triangles excluded) and ghost crossings per state
-__device__ Seg2 seg2(const DevScene& S, float3 a, float3 b, int ea, int eb, bool want0, bool want1, QCount& qc) {
-  Seg2 r;
-  r.vis[0] = r.vis[1] = false;
-  r.c[0] = r.c[1] = cross_zero();
-  float3 dv = b - a;
-  float L = sqrtf(dot3(dv, dv));
-  if (!(L > 2.0f * S.eps)) return r;
-  float3 d = dv * (1.0f / L);
-  WRay wr = make_wray(a, d);
-  bool sblock = occluded_static(S, wr, S.eps, L - S.eps, ea, eb);
-  qc.shadow++;
-  for (int F = 0; F < 2; ++F) {
-    if (!(F == 0 ? want0 : want1)) continue;
-    r.vis[F] = !sblock && !occluded_dyn(S, F, a, d, S.eps, L - S.eps, ea, eb);
-    if (S.n_moved > 0) {
-      r.c[F] = crossings(S, F, a, d, S.eps, L - S.eps, L);
-      qc.inst++;
-    }
-  }
-  return r;
-}
-__device__ __forceinline__ Cross swapc(Cross c) {
-  float t = c.sa;
-  c.sa = c.sb;
-  c.sb = t;
-  return c;
-}
-
-// area pdf of generating `to` from `from` with the walk arriving from `prev` (state F)
-__device__ __forceinline__ float area_pdf(const DevScene& S, int F, const PV& prev, const PV& from, const PV& to) {
-  Mat m = load_mat(S, (uint32_t)from.obj, F);
-  float3 wi = norm3_exact(prev.p - from.p);
-  float3 dv = to.p - from.p;
-  float d2 = dot3(dv, dv);
-  float3 wo = dv * (1.0f / sqrtf(d2));
-  return bsdf_pdf(m, from.n, wi, wo) * fabsf(dot3(to.n, wo)) / d2;
-}
-
-// ------------------------------------------------------------------------------------------------
-// value of a connection path v = f / Pi (Eq.2; balance heuristic P:L351-353), in state F.
-// x[0] = E, x[k-1] = L; e[i] = crossings of edge (x_i, x_{i+1}) with sa measured from x_i, sb from x_{i+1}.
-// Computed as (f / p_T7) / (1 + sum_c p_c / p_T7).
-// ------------------------------------------------------------------------------------------------
-__device__ float3 path_value(const DevScene& S, const PV* x, const Cross* e, int k, int F, uint32_t mask) {
-  const float3 zero = f3(0.f, 0.f, 0.f);
-  float3 d01 = x[1].p - x[0].p;
-  float dd01 = dot3(d01, d01);
-  float3 w01 = d01 * (1.0f / sqrtf(dd01));
-  float cth = dot3(w01, S.cf);
-  if (!(cth > 0.0f)) return zero;
-  const PV& L = x[k - 1];
-  float4 le4 = __ldg(&S.obj_emit[L.obj]);
-  float3 Le = f3(le4.x, le4.y, le4.z);
-  if (!(dot3(L.n, x[k - 2].p - L.p) > 0.0f)) return zero;  // front face only
-  if (k == 2) return Le;                                     // direct view: W_e G / p_cam = 1, Pi = p_T7
-  float cos1 = fabsf(dot3(x[1].n, w01));
-  float invpcam = S.Aplane * cth * cth * cth * dd01 / cos1;  // 1 / p_cam(x_1)
-  float pL = __ldg(&S.emit_pL[__ldg(&S.obj_emitter[L.obj])]);
-  const bool t1 = mask & 1u, t2 = mask & 2u, t3 = mask & 4u, t4 = mask & 8u, t5 = mask & 16u, t6 = mask & 32u;
-  float3 T = f3(1.f, 1.f, 1.f);
-  float sum = 1.0f;  // T7
-  if (t5 && e[0].n > 0.0f) sum += S.pA_G * S.Aplane * cth * cth * cth * e[0].sa;
-  float Q = 1.0f;  // prod_{m < i} rev_m / fwd_{m+1}
-  for (int i = 1; i <= k - 2; ++i) {
-    Mat m = load_mat(S, (uint32_t)x[i].obj, F);
-    float3 wi = norm3_exact(x[i - 1].p - x[i].p);
-    float3 dv = x[i + 1].p - x[i].p;
-    float d2 = dot3(dv, dv);
-    float3 wo = dv * (1.0f / sqrtf(d2));
-    float3 rho = bsdf_eval(m, x[i].n, wi, wo);
-    float pf = bsdf_pdf(m, x[i].n, wi, wo);
-    float cout = fabsf(dot3(x[i].n, wo));
-    float cin_next = fabsf(dot3(x[i + 1].n, wo));
-    bool dyn = edited(S, x[i].obj);
-    if (!(pf > 0.0f)) return zero;  // f = 0 (rho = 0 exactly where pf = 0 for these BSDFs)
-    if (i < k - 2) {
-      T = mul3(T, rho * (cout / pf));
-    } else {
-      T = mul3(mul3(T, rho), Le) * (cout * cin_next / d2 / pL);
-    }
-    float base = S.pA_D * invpcam * Q;
-    if (dyn) {
-      if (i == k - 2) { if (t1) sum += base; }                          // T1: adjacent to the emitter
-      else if (i == 1) { if (t2) sum += S.pA_D * invpcam; }             // T2: adjacent to the sensor
-      else if (t3) sum += base * (fmaxf(0.0f, dot3(x[i].n, wo)) * RR_INV_PI_F) / pf;  // T3
-    }
-    if (e[i].n > 0.0f) {
-      if (i + 1 == k - 1) { if (t4) sum += S.pA_G * e[i].sb * cout / d2 * invpcam * Q; }  // T4 (Eq. vertex1pdf)
-      else if (t6) sum += S.pA_G * (0.25f * RR_INV_PI_F) * e[i].s0 * cout / pf * invpcam * Q;  // T6
-    }
-    if (i <= k - 3) {  // q_i = rev_i / fwd_{i+1} on edge (i, i+1)
-      Mat mn = load_mat(S, (uint32_t)x[i + 1].obj, F);
-      float pr = bsdf_pdf(mn, x[i + 1].n, norm3_exact(x[i + 2].p - x[i + 1].p), wo * -1.0f);
-      Q *= pr * cout / (pf * cin_next);
-    }
-  }
-  return T * (1.0f / sum);
-}
-
-// ------------------------------------------------------------------------------------------------
-// splat + records + statistics
-// ------------------------------------------------------------------------------------------------
-struct Out {
-  const KArgs* A;
-  QCount qc;
-  uint32_t conns, acc, rej, unp, monly, recon, splats, offscreen, zero;
-  uint32_t rejby[6];
-};
-__device__ __forceinline__ void splat(Out& o, int pix, float3 t) {
-  if (t.x == 0.0f && t.y == 0.0f && t.z == 0.0f) return;
-  if (pix < 0) {
-    o.offscreen++;
-    return;
-  }
-  o.splats++;
-  atomicAdd(reinterpret_cast<float4*>(o.A->image) + pix, make_float4(t.x, t.y, t.z, 0.0f));
-}
-__device__ void emit_record(Out& o, uint64_t i, int kind, int a, int b, int status, int reason, int pix_p, float3 tp,
-                            int pix_q, float3 tq, float R) {
-  const KArgs& A = *o.A;
-  if (status == ST_ACCEPTED) o.acc++;
-  else if (status == ST_REJECTED) { o.rej++; o.rejby[reason < 6 ? reason : 0]++; }
-  else if (status == ST_UNPAIRED) o.unp++;
-  else o.monly++;
-  if (status != ST_MAPPED_ONLY) o.conns++;
-  if (pix_p == pix_q) {
-    float3 s = tp + tq;
-    if (s.x == 0.0f && s.y == 0.0f && s.z == 0.0f && (tp.x != 0.0f || tp.y != 0.0f || tp.z != 0.0f)) o.zero++;
-    if (!A.dump) splat(o, pix_p, s);
-  } else if (!A.dump) {
-    splat(o, pix_p, tp);
-    splat(o, pix_q, tq);
-  }
-  if (A.dump) {
-    unsigned long long slot = atomicAdd(A.rec_count, 1ull);
-    if (slot < A.rec_cap) {
-      rr_path_record r;
-      r.tech = A.tech;
-      r.side = A.side;
-      r.i = i;
-      r.key_kind = kind;
-      r.key_a = a;
-      r.key_b = b;
-      r.status = status;
-      r.reason = reason;
-      r.pix_p = pix_p;
-      r.term_p[0] = tp.x; r.term_p[1] = tp.y; r.term_p[2] = tp.z;
-      r.pix_q = pix_q;
-      r.term_q[0] = tq.x; r.term_q[1] = tq.y; r.term_q[2] = tq.z;
-      r.R = R;
-      A.recs[slot] = r;
-    }
-  }
-}
-// terms of one connection pair and splat
-__device__ void finish(Out& o, uint64_t i, int kind, int a, int b, int status, int reason, int pix_p, float3 vp,
-                       int pix_q, float3 vq, float R) {
-  const KArgs& A = *o.A;
-  float3 tp, tq;
-  if (A.two_way) {
-    float wgt = (status == ST_ACCEPTED) ? 1.0f : 2.0f;
-    tp = vp * (wgt * A.sigma * A.inv_spp);
-    tq = (status == ST_ACCEPTED) ? vq * (-A.sigma * A.inv_spp * R) : f3(0.f, 0.f, 0.f);
-    if (status != ST_ACCEPTED) pix_q = -1;
-  } else {
-    tp = vp * A.inv_spp;
-    tq = vq * (-A.inv_spp);
-  }
-  emit_record(o, i, kind, a, b, status, reason, pix_p, tp, pix_q, tq, R);
-}
+__device__ __forceinline__ int bit(int F) { return 1 << F; }
 
 // ------------------------------------------------------------------------------------------------
 // single-walk techniques: T7, T1, T2, T4, T5  (E-rooted: T7, T2, T5; L-rooted: T1, T4)
 // ------------------------------------------------------------------------------------------------
-struct Walk {
+struct SWalk {
   PV v[RR_MAXV];
   Cross ex[RR_MAXV];  // ex[m]: crossings of the walk edge v[m-1] -> v[m], sa measured from v[m-1]
   int n;              // number of walk vertices (0: the technique failed)
   int pixel;          // fixed pixel (T7, T2, T5)
 };
+struct SStart {  // start element of one side, kept between issue and consume
+  PV a, b;
+  float dl;
+  float3 dir;
+  int pix, qi;
+};
+struct SState {
+  uint64_t i;
+  Rng rng;
+  int pc, m;
+  SWalk P, Q;
+  SStart sp, sq;
+  int recon, w, reject_from, reject_reason;  // recon: 0 none, 1 reconnected, 2 failed, 3 pending visibility
+  float R1, R2;
+  bool rdiv, hdiv, Pend, Qend, suffix_pending;
+  int dynP, dynQ;
+  // temporaries of the current step
+  int q_recon, q_suffix, q_cp, q_cq, q_wp, q_wq;
+  bool pc_, qc_, okP, okQ, walk_shared, attempt, qActive, div_m, has_conn;
+  PV L;
+  int pixp, pixq;
+  float3 woP, woQ;
+};
 
-// start of a single-walk technique in state F (C4).  For T7 the caller traces both states.
-__device__ void start_single(const DevScene& S, int tech, int F, const float d0[8], const KArgs& A, uint64_t i,
-                             Walk& W, QCount& qc) {
-  W.n = 0;
-  W.pixel = -1;
+__device__ __forceinline__ bool nee_ok(int tech, int m) { return tech == 2 ? m >= 2 : true; }
+
+// issue the start query of one side
+__device__ void start_issue(const DevScene& S, int tech, int F, const float d0[8], SStart& s, Batch& B) {
+  s.qi = -1;
   PV E = cam_pv(S);
   switch (tech) {
-    case 1: {  // dynamic from emitter
+    case 1: {  // dynamic from emitter: x_D, x_L, "fails if blocked"
       if (S.n_edited == 0) return;
-      PV xd = sample_set(S, S.edited_tris, S.edited_cdf, S.n_edited, F, d0[0], d0[1], d0[2]);
-      PV xl = sample_emitter(S, d0[3], d0[4], d0[5], d0[6]);
-      if (!(dot3(xl.n, xd.p - xl.p) > 0.0f)) return;
-      Seg2 s = seg2(S, xl.p, xd.p, xl.tri, xd.tri, F == 0, F == 1, qc);  // "fails if blocked"
-      if (!s.vis[F]) return;
-      W.v[0] = xl; W.v[1] = xd; W.ex[1] = s.c[F]; W.n = 1;
+      s.b = sample_set(S, S.edited_tris, S.edited_cdf, S.n_edited, F, d0[0], d0[1], d0[2]);
+      s.a = sample_emitter(S, d0[3], d0[4], d0[5], d0[6]);
+      if (!(dot3(s.a.n, s.b.p - s.a.p) > 0.0f)) return;
+      s.qi = B.push(mk_seg(s.a.p, s.b.p, s.a.tri, s.b.tri, bit(F)));
       return;
     }
     case 2: {  // dynamic from sensor
       if (S.n_edited == 0) return;
-      PV xd = sample_set(S, S.edited_tris, S.edited_cdf, S.n_edited, F, d0[0], d0[1], d0[2]);
-      int pix = project(S, xd.p);
-      if (pix < 0) return;
-      Seg2 s = seg2(S, E.p, xd.p, -1, xd.tri, F == 0, F == 1, qc);
-      if (!s.vis[F]) return;
-      W.v[0] = E; W.v[1] = xd; W.ex[1] = s.c[F]; W.n = 1; W.pixel = pix;
+      s.b = sample_set(S, S.edited_tris, S.edited_cdf, S.n_edited, F, d0[0], d0[1], d0[2]);
+      s.pix = project(S, s.b.p);
+      if (s.pix < 0) return;
+      s.qi = B.push(mk_seg(E.p, s.b.p, -1, s.b.tri, bit(F)));
       return;
     }
     case 4: {  // ghost from emitter: x_G on ghost_F = moved objects at M_Fbar
       if (S.n_moved == 0) return;
       PV xg = sample_set(S, S.moved_tris, S.moved_cdf, S.n_moved, 1 - F, d0[0], d0[1], d0[2]);
-      PV xl = sample_emitter(S, d0[3], d0[4], d0[5], d0[6]);
-      float3 dv = xg.p - xl.p;
-      float dl = sqrtf(dot3(dv, dv));
-      if (!(dl > S.eps)) return;
-      float3 dir = dv * (1.0f / dl);
-      if (!(dot3(xl.n, dir) > 0.0f)) return;
-      Trace2 t = trace2(S, xl.p, dir, xl.tri, F == 0, F == 1, qc);
-      if (!t.ok[F]) return;
-      float3 q = t.v[F].p - xl.p;
-      if (!(sqrtf(dot3(q, q)) > dl + S.eps)) return;
-      W.v[0] = xl; W.v[1] = t.v[F]; W.ex[1] = t.c[F]; W.n = 1;
+      s.a = sample_emitter(S, d0[3], d0[4], d0[5], d0[6]);
+      float3 dv = xg.p - s.a.p;
+      s.dl = sqrtf(dot3(dv, dv));
+      if (!(s.dl > S.eps)) return;
+      s.dir = dv * (1.0f / s.dl);
+      if (!(dot3(s.a.n, s.dir) > 0.0f)) return;
+      s.qi = B.push(mk_ray(s.a.p, s.dir, s.a.tri, bit(F)));
       return;
     }
     case 5: {  // ghost from sensor
       if (S.n_moved == 0) return;
       PV xg = sample_set(S, S.moved_tris, S.moved_cdf, S.n_moved, 1 - F, d0[0], d0[1], d0[2]);
-      int pix = project(S, xg.p);
-      if (pix < 0) return;
+      s.pix = project(S, xg.p);
+      if (s.pix < 0) return;
       float3 dv = xg.p - E.p;
-      float dg = sqrtf(dot3(dv, dv));
-      float3 dir = dv * (1.0f / dg);
-      Trace2 t = trace2(S, E.p, dir, -1, F == 0, F == 1, qc);
-      if (!t.ok[F]) return;
-      float3 q = t.v[F].p - E.p;
-      if (!(sqrtf(dot3(q, q)) > dg + S.eps)) return;
-      W.v[0] = E; W.v[1] = t.v[F]; W.ex[1] = t.c[F]; W.n = 1; W.pixel = pix;
+      s.dl = sqrtf(dot3(dv, dv));
+      s.dir = dv * (1.0f / s.dl);
+      s.qi = B.push(mk_ray(E.p, s.dir, -1, bit(F)));
       return;
     }
   }
 }
-
-__device__ __forceinline__ bool nee_ok(int tech, int m) { return tech == 2 ? m >= 2 : true; }
-
-__device__ void sample_single(const DevScene& S, const KArgs& A, uint64_t i, const Rng& rng, Out& o) {
-  const int F = A.side, Fb = 1 - A.side;
-  const int l = A.tech, lq = A.tech_q;
-  const int D = A.max_depth;
-  const bool Lroot = (l == 1 || l == 4);
-  float d0[8];
-  rng.dims(0, d0);
-  Walk P, Q;
+__device__ void start_consume(const DevScene& S, int tech, int F, const SStart& s, const Batch& B, SWalk& W) {
+  W.n = 0;
+  W.pixel = -1;
+  if (s.qi < 0) return;
+  const QRes& r = B.r[s.qi];
   PV E = cam_pv(S);
-  if (l == 7) {  // same pixel and jitter in both states: one trace serves both (A3)
-    int npix = S.W * S.H;
-    int pix = (int)(i % (uint64_t)npix);
-    float3 dir = camera_dir(S, (float)(pix % S.W) + d0[0], (float)(pix / S.W) + d0[1]);
-    Trace2 t = trace2(S, E.p, dir, -1, true, true, o.qc);
-    P.n = Q.n = 0;
-    P.pixel = Q.pixel = pix;
-    if (t.ok[F]) { P.v[0] = E; P.v[1] = t.v[F]; P.ex[1] = t.c[F]; P.n = 1; }
-    if (t.ok[Fb]) { Q.v[0] = E; Q.v[1] = t.v[Fb]; Q.ex[1] = t.c[Fb]; Q.n = 1; }
+  if (tech == 1 || tech == 2) {
+    if (!r.ok[F]) return;
+    W.v[0] = tech == 1 ? s.a : E;
+    W.v[1] = s.b;
+    W.ex[1] = r.c[F];
+    W.n = 1;
+    W.pixel = tech == 2 ? s.pix : -1;
   } else {
-    start_single(S, l, F, d0, A, i, P, o.qc);
-    start_single(S, lq, Fb, d0, A, i, Q, o.qc);
+    if (!r.ok[F]) return;
+    float3 o = tech == 4 ? s.a.p : E.p;
+    PV h = hit_pv(S, r.h[F], o, s.dir, F);
+    float3 q = h.p - o;
+    if (!(sqrtf(dot3(q, q)) > s.dl + S.eps)) return;  // the first hit lies beyond x_G
+    W.v[0] = tech == 4 ? s.a : E;
+    W.v[1] = h;
+    W.ex[1] = r.c[F];
+    W.n = 1;
+    W.pixel = tech == 5 ? s.pix : -1;
   }
-  if (P.n == 0 && (A.two_way || Q.n == 0)) return;
+}
 
-  const int maxW = D - 1 > 1 ? D - 1 : 1;  // walk vertices needed (connections at j <= D-1; T7 emission at 1)
-  int recon = 0;                            // 0 none, 1 reconnected at w, 2 failed at w
-  int w = 0;
-  int reject_from = 1 << 30, reject_reason = RJ_NONE;
-  float R1 = 1.0f, R2 = 1.0f;
-  bool rdiv = false, hdiv = false;
-  int dynP = 0, dynQ = 0;
-  bool Pend = P.n == 0, Qend = Q.n == 0;
-
-  for (int m = 1;; ++m) {
-    bool hasP = m <= P.n, hasQ = m <= Q.n;
-    if (!hasP && (A.two_way || !hasQ)) break;
-    bool vdiff = hasP && hasQ && !same_pv(S, P.v[m], Q.v[m]);
-    hdiv = hdiv || vdiff || (hasP != hasQ);
-    if (hasP && edited(S, P.v[m].obj)) dynP++;
-    if (hasQ && edited(S, Q.v[m].obj)) dynQ++;
-
-    // ---------------- connections at walk vertex m
+// issue the queries of walk vertex m (connection at m, walk step from m, pending reconnection/suffix checks)
+__device__ void single_issue(const DevScene& S, const KArgs& A, SState& st, Batch& B) {
+  const int F = A.side, Fb = 1 - F, l = A.tech, lq = A.tech_q, D = A.max_depth, m = st.m;
+  const bool Lroot = (l == 1 || l == 4);
+  const int maxW = D - 1 > 1 ? D - 1 : 1;
+  SWalk& P = st.P;
+  SWalk& Q = st.Q;
+  PV E = cam_pv(S);
+  st.q_recon = st.q_suffix = st.q_cp = st.q_cq = st.q_wp = st.q_wq = -1;
+  bool hasP = m <= P.n, hasQ = m <= Q.n;
+  bool vdiff = hasP && hasQ && !same_pv(S, P.v[m], Q.v[m]);
+  st.hdiv = st.hdiv || vdiff || (hasP != hasQ);
+  if (hasP && edited(S, P.v[m].obj)) st.dynP++;
+  if (hasQ && edited(S, Q.v[m].obj)) st.dynQ++;
+  if (st.recon == 3) st.q_recon = B.push(mk_seg(Q.v[st.w].p, P.v[st.w + 1].p, Q.v[st.w].tri, P.v[st.w + 1].tri, bit(Fb)));
+  if (st.suffix_pending) st.q_suffix = B.push(mk_seg(P.v[m - 1].p, P.v[m].p, P.v[m - 1].tri, P.v[m].tri, bit(Fb), true));
+  float d[8];
+  st.rng.dims((uint32_t)m, d);
+  // ---- connection at m
+  st.has_conn = false;
+  st.pc_ = st.qc_ = false;
+  if (m + 1 <= D) {
+    bool failed_q = (st.recon == 2 && m >= st.w + 1);
     if (!Lroot) {
-      // direct view of an emitter (T7 only, k = 2)
-      if (l == 7 && m == 1) {
-        bool pe = hasP && __ldg(&S.obj_emitter[P.v[1].obj]) >= 0;
-        bool qe = hasQ && __ldg(&S.obj_emitter[Q.v[1].obj]) >= 0;
-        PV x[2];
-        Cross ce[1];
-        float3 vp = f3(0.f, 0.f, 0.f), vq = vp;
-        if (pe) { x[0] = E; x[1] = P.v[1]; ce[0] = P.ex[1]; vp = path_value(S, x, ce, 2, F, A.mask); }
-        if (qe) { x[0] = E; x[1] = Q.v[1]; ce[0] = Q.ex[1]; vq = path_value(S, x, ce, 2, Fb, A.mask); }
-        if (pe) {
-          int st = qe ? ST_ACCEPTED : ST_UNPAIRED;
-          if (st == ST_ACCEPTED && A.reject_multi && hdiv && (dynP >= 2 || dynQ >= 2)) st = ST_REJECTED;
-          finish(o, i, 0, 1, 0, st, st == ST_REJECTED ? RJ_MULTI : RJ_NONE, P.pixel, vp, Q.pixel, vq, 1.0f);
-        } else if (qe && !A.two_way) {
-          finish(o, i, 0, 1, 0, ST_MAPPED_ONLY, RJ_NONE, -1, f3(0.f, 0.f, 0.f), Q.pixel, vq, 1.0f);
-        }
-      }
-      // NEE at v_m: path (E, v_1..v_m, L), slot m
-      if (m + 1 <= D) {
-        bool pc = hasP && nee_ok(l, m);
-        bool reconnected_here = (recon == 1 && m >= w + 1);
-        bool qc_ = hasQ && nee_ok(lq, m) && !(recon == 2 && m >= w + 1);
-        if (reconnected_here && m >= reject_from) qc_ = false;
-        if (pc || (qc_ && !A.two_way)) {
-          float d[8];
-          rng.dims((uint32_t)m, d);
-          PV L = sample_emitter(S, d[3], d[4], d[5], d[6]);
-          Seg2 sp, sq;
-          bool shared = pc && qc_ && same_pv(S, P.v[m], Q.v[m]);
-          if (shared) {
-            sp = seg2(S, P.v[m].p, L.p, P.v[m].tri, L.tri, true, true, o.qc);
-            sq = sp;
-          } else {
-            if (pc) sp = seg2(S, P.v[m].p, L.p, P.v[m].tri, L.tri, F == 0, F == 1, o.qc);
-            if (qc_) sq = seg2(S, Q.v[m].p, L.p, Q.v[m].tri, L.tri, Fb == 0, Fb == 1, o.qc);
-          }
-          PV x[RR_MAXV + 1];
-          Cross ce[RR_MAXV + 1];
-          float3 vp = f3(0.f, 0.f, 0.f), vq = vp;
-          if (pc && sp.vis[F]) {
-            x[0] = E;
-            for (int j = 1; j <= m; ++j) { x[j] = P.v[j]; ce[j - 1] = P.ex[j]; }
-            x[m + 1] = L;
-            ce[m] = sp.c[F];
-            vp = path_value(S, x, ce, m + 2, F, A.mask);
-          }
-          if (qc_ && sq.vis[Fb]) {
-            x[0] = E;
-            for (int j = 1; j <= m; ++j) { x[j] = Q.v[j]; ce[j - 1] = Q.ex[j]; }
-            x[m + 1] = L;
-            ce[m] = sq.c[Fb];
-            vq = path_value(S, x, ce, m + 2, Fb, A.mask);
-          }
-          if (pc) {
-            int st = ST_ACCEPTED, rs = RJ_NONE;
-            float R = 1.0f;
-            if (recon == 2 && m >= w + 1) { st = ST_REJECTED; rs = reject_reason; }
-            else if (reconnected_here && m >= reject_from) { st = ST_REJECTED; rs = reject_reason; }
-            else if (!qc_) st = ST_UNPAIRED;
-            else if (reconnected_here) {
-              R = R1 * (m >= w + 2 ? R2 : 1.0f);
-              if (!(R > 0.0f) || !isfinite(R)) { st = ST_REJECTED; rs = RJ_TARGET; }
-            }
-            if (st == ST_ACCEPTED && A.reject_multi && hdiv && (dynP >= 2 || dynQ >= 2)) { st = ST_REJECTED; rs = RJ_MULTI; }
-            finish(o, i, 1, m, 0, st, rs, P.pixel, vp, Q.pixel, vq, R);
-          } else if (qc_ && !A.two_way) {
-            finish(o, i, 1, m, 0, ST_MAPPED_ONLY, RJ_NONE, -1, f3(0.f, 0.f, 0.f), Q.pixel, vq, 1.0f);
-          }
-        }
-      }
-    } else if (m + 1 <= D) {
-      // sensor connection at v_m: path (E, v_m..v_1, x_L)
-      bool pc = hasP;
-      bool reconnected_here = (recon == 1 && m >= w + 1);
-      bool qc_ = hasQ && !(recon == 2 && m >= w + 1);
-      if (reconnected_here && m >= reject_from) qc_ = false;
-      if (pc || (qc_ && !A.two_way)) {
-        Seg2 sp, sq;
-        int pixp = -1, pixq = -1;
-        bool shared = pc && qc_ && same_pv(S, P.v[m], Q.v[m]);
-        if (pc) pixp = project(S, P.v[m].p);
-        if (qc_) pixq = project(S, Q.v[m].p);
+      st.pc_ = hasP && nee_ok(l, m);
+      st.qc_ = hasQ && nee_ok(lq, m) && !failed_q;
+      if (st.pc_ || (st.qc_ && !A.two_way)) {
+        st.has_conn = true;
+        st.L = sample_emitter(S, d[3], d[4], d[5], d[6]);
+        bool shared = st.pc_ && st.qc_ && same_pv(S, P.v[m], Q.v[m]);
         if (shared) {
-          sp = seg2(S, P.v[m].p, E.p, P.v[m].tri, -1, true, true, o.qc);
-          sq = sp;
+          st.q_cp = st.q_cq = B.push(mk_seg(P.v[m].p, st.L.p, P.v[m].tri, st.L.tri, 3));
         } else {
-          if (pc) sp = seg2(S, P.v[m].p, E.p, P.v[m].tri, -1, F == 0, F == 1, o.qc);
-          if (qc_) sq = seg2(S, Q.v[m].p, E.p, Q.v[m].tri, -1, Fb == 0, Fb == 1, o.qc);
+          if (st.pc_) st.q_cp = B.push(mk_seg(P.v[m].p, st.L.p, P.v[m].tri, st.L.tri, bit(F)));
+          if (st.qc_) st.q_cq = B.push(mk_seg(Q.v[m].p, st.L.p, Q.v[m].tri, st.L.tri, bit(Fb)));
         }
-        PV x[RR_MAXV + 1];
-        Cross ce[RR_MAXV + 1];
-        float3 vp = f3(0.f, 0.f, 0.f), vq = vp;
-        if (pc && sp.vis[F]) {
-          x[0] = E;
-          ce[0] = swapc(sp.c[F]);
-          for (int j = 1; j <= m; ++j) { x[j] = P.v[m + 1 - j]; ce[j] = swapc(P.ex[m + 1 - j]); }
-          x[m + 1] = P.v[0];
-          vp = path_value(S, x, ce, m + 2, F, A.mask);
-        }
-        if (qc_ && sq.vis[Fb]) {
-          x[0] = E;
-          ce[0] = swapc(sq.c[Fb]);
-          for (int j = 1; j <= m; ++j) { x[j] = Q.v[m + 1 - j]; ce[j] = swapc(Q.ex[m + 1 - j]); }
-          x[m + 1] = Q.v[0];
-          vq = path_value(S, x, ce, m + 2, Fb, A.mask);
-        }
-        if (pc) {
-          int st = ST_ACCEPTED, rs = RJ_NONE;
-          float R = 1.0f;
-          if (recon == 2 && m >= w + 1) { st = ST_REJECTED; rs = reject_reason; }
-          else if (reconnected_here && m >= reject_from) { st = ST_REJECTED; rs = reject_reason; }
-          else if (!qc_) st = ST_UNPAIRED;
-          else if (reconnected_here) {
-            R = R1 * (m >= w + 2 ? R2 : 1.0f);
-            if (!(R > 0.0f) || !isfinite(R)) { st = ST_REJECTED; rs = RJ_TARGET; }
-          }
-          if (st == ST_ACCEPTED && A.reject_multi && hdiv && (dynP >= 2 || dynQ >= 2)) { st = ST_REJECTED; rs = RJ_MULTI; }
-          finish(o, i, 2, m, 0, st, rs, pixp, vp, pixq, vq, R);
-        } else if (qc_ && !A.two_way) {
-          finish(o, i, 2, m, 0, ST_MAPPED_ONLY, RJ_NONE, -1, f3(0.f, 0.f, 0.f), pixq, vq, 1.0f);
+      }
+    } else {
+      st.pc_ = hasP;
+      st.qc_ = hasQ && !failed_q;
+      if (st.pc_ || (st.qc_ && !A.two_way)) {
+        st.has_conn = true;
+        st.pixp = st.pc_ ? project(S, P.v[m].p) : -1;
+        st.pixq = st.qc_ ? project(S, Q.v[m].p) : -1;
+        bool shared = st.pc_ && st.qc_ && same_pv(S, P.v[m], Q.v[m]);
+        if (shared) {
+          st.q_cp = st.q_cq = B.push(mk_seg(P.v[m].p, E.p, P.v[m].tri, -1, 3));
+        } else {
+          if (st.pc_) st.q_cp = B.push(mk_seg(P.v[m].p, E.p, P.v[m].tri, -1, bit(F)));
+          if (st.qc_) st.q_cq = B.push(mk_seg(Q.v[m].p, E.p, Q.v[m].tri, -1, bit(Fb)));
         }
       }
     }
-    if (m >= maxW) break;
-
-    // ---------------- advance the walks from v_m (slot m)
-    float d[8];
-    rng.dims((uint32_t)m, d);
-    bool qActive = (recon == 0) && hasQ && !Qend;
-    bool okP = false, okQ = false;
-    float3 woP, woQ;
+  }
+  // ---- walk step from v_m (slot m)
+  st.okP = st.okQ = st.walk_shared = st.attempt = false;
+  st.qActive = (st.recon == 0) && hasQ && !st.Qend;
+  st.div_m = st.rdiv || vdiff;
+  if (m < maxW) {
     Mat mp, mq;
-    if (hasP && !Pend) {
+    if (hasP && !st.Pend) {
       mp = load_mat(S, (uint32_t)P.v[m].obj, F);
-      okP = bsdf_sample(mp, P.v[m].n, norm3_exact(P.v[m - 1].p - P.v[m].p), d[1], d[2], woP);
+      st.okP = bsdf_sample(mp, P.v[m].n, norm3_exact(P.v[m - 1].p - P.v[m].p), d[1], d[2], st.woP);
     }
-    if (qActive) {
+    if (st.qActive) {
       mq = load_mat(S, (uint32_t)Q.v[m].obj, Fb);
-      okQ = bsdf_sample(mq, Q.v[m].n, norm3_exact(Q.v[m - 1].p - Q.v[m].p), d[1], d[2], woQ);
+      st.okQ = bsdf_sample(mq, Q.v[m].n, norm3_exact(Q.v[m - 1].p - Q.v[m].p), d[1], d[2], st.woQ);
     }
-    bool dirdiv = qActive && hasP && !Pend && ((okP != okQ) || (okP && okQ && !eq3(woP, woQ)));
-    bool div_m = rdiv || vdiff || dirdiv;
-    bool shared = qActive && okP && okQ && !vdiff && !dirdiv;
-    bool gotP = false;
-    if (okP) {
-      Trace2 t = trace2(S, P.v[m].p, woP, P.v[m].tri, F == 0 || shared, F == 1 || shared, o.qc);
-      if (t.ok[F]) { P.v[m + 1] = t.v[F]; P.ex[m + 1] = t.c[F]; P.n = m + 1; gotP = true; }
-      if (shared) {
-        if (t.ok[Fb]) { Q.v[m + 1] = t.v[Fb]; Q.ex[m + 1] = t.c[Fb]; Q.n = m + 1; }
-        else Qend = true;
+    bool dirdiv = st.qActive && hasP && !st.Pend && ((st.okP != st.okQ) || (st.okP && st.okQ && !eq3(st.woP, st.woQ)));
+    st.div_m = st.rdiv || vdiff || dirdiv;
+    st.walk_shared = st.qActive && st.okP && st.okQ && !vdiff && !dirdiv;
+    st.attempt = A.reconnect && st.recon == 0 && st.qActive && hasP && st.div_m && rough_enough(mp, A.alpha_min) &&
+                 rough_enough(mq, A.alpha_min);
+    if (st.okP) st.q_wp = B.push(mk_ray(P.v[m].p, st.woP, P.v[m].tri, bit(F) | (st.walk_shared ? bit(Fb) : 0)));
+    if (st.qActive && st.okQ && !st.walk_shared && !st.attempt)
+      st.q_wq = B.push(mk_ray(Q.v[m].p, st.woQ, Q.v[m].tri, bit(Fb)));
+  }
+}
+
+// consume the results of walk vertex m; returns false when the sample is finished
+__device__ bool single_consume(const DevScene& S, const KArgs& A, SState& st, const Batch& B, Out& o) {
+  const int F = A.side, Fb = 1 - F, l = A.tech, D = A.max_depth, m = st.m;
+  const bool Lroot = (l == 1 || l == 4);
+  const int maxW = D - 1 > 1 ? D - 1 : 1;
+  SWalk& P = st.P;
+  SWalk& Q = st.Q;
+  PV E = cam_pv(S);
+  const uint64_t i = st.i;
+  bool hasP = m <= P.n, hasQ = m <= Q.n;
+  // ---- pending reconnection edge (checked in View_Fbar)
+  if (st.q_recon >= 0) {
+    const QRes& r = B.r[st.q_recon];
+    if (!r.ok[Fb]) {
+      st.recon = 2;
+      if (st.w + 1 < st.reject_from) { st.reject_from = st.w + 1; st.reject_reason = RJ_OCCLUDED; }
+    } else {
+      st.recon = 1;
+      Q.ex[st.w + 1] = r.c[Fb];
+      o.recon++;
+    }
+  }
+  // ---- shared suffix edge v_{m-1} -> v_m re-checked against dyn_Fbar only
+  if (st.q_suffix >= 0) {
+    const QRes& r = B.r[st.q_suffix];
+    if (!r.ok[Fb] && m < st.reject_from) { st.reject_from = m; st.reject_reason = RJ_OCCLUDED; }
+    Q.ex[m] = r.c[Fb];
+    st.suffix_pending = false;
+  }
+  // ---- direct view of an emitter (T7 only, k = 2)
+  if (l == 7 && m == 1) {
+    bool pe = hasP && __ldg(&S.obj_emitter[P.v[1].obj]) >= 0;
+    bool qe = hasQ && __ldg(&S.obj_emitter[Q.v[1].obj]) >= 0;
+    PV x[2];
+    Cross ce[1];
+    float3 vp = f3(0.f, 0.f, 0.f), vq = vp;
+    if (pe) { x[0] = E; x[1] = P.v[1]; ce[0] = P.ex[1]; vp = path_value(S, x, ce, 2, F, A.mask); }
+    if (qe) { x[0] = E; x[1] = Q.v[1]; ce[0] = Q.ex[1]; vq = path_value(S, x, ce, 2, Fb, A.mask); }
+    if (pe) {
+      int stt = qe ? ST_ACCEPTED : ST_UNPAIRED;
+      if (stt == ST_ACCEPTED && A.reject_multi && st.hdiv && (st.dynP >= 2 || st.dynQ >= 2)) stt = ST_REJECTED;
+      finish(o, i, 0, 1, 0, stt, stt == ST_REJECTED ? RJ_MULTI : RJ_NONE, P.pixel, vp, Q.pixel, vq, 1.0f);
+    } else if (qe && !A.two_way) {
+      finish(o, i, 0, 1, 0, ST_MAPPED_ONLY, RJ_NONE, -1, f3(0.f, 0.f, 0.f), Q.pixel, vq, 1.0f);
+    }
+  }
+  // ---- connection at m
+  if (st.has_conn) {
+    const bool reconnected_here = (st.recon == 1 && m >= st.w + 1);
+    bool qc_ = st.qc_ && !(st.recon == 2 && m >= st.w + 1) && !(reconnected_here && m >= st.reject_from);
+    PV x[RR_MAXV + 1];
+    Cross ce[RR_MAXV + 1];
+    float3 vp = f3(0.f, 0.f, 0.f), vq = vp;
+    int pixp, pixq;
+    if (!Lroot) {
+      pixp = P.pixel;
+      pixq = Q.pixel;
+      if (st.pc_ && B.r[st.q_cp].ok[F]) {
+        x[0] = E;
+        for (int j = 1; j <= m; ++j) { x[j] = P.v[j]; ce[j - 1] = P.ex[j]; }
+        x[m + 1] = st.L;
+        ce[m] = B.r[st.q_cp].c[F];
+        vp = path_value(S, x, ce, m + 2, F, A.mask);
+      }
+      if (qc_ && B.r[st.q_cq].ok[Fb]) {
+        x[0] = E;
+        for (int j = 1; j <= m; ++j) { x[j] = Q.v[j]; ce[j - 1] = Q.ex[j]; }
+        x[m + 1] = st.L;
+        ce[m] = B.r[st.q_cq].c[Fb];
+        vq = path_value(S, x, ce, m + 2, Fb, A.mask);
+      }
+    } else {
+      pixp = st.pixp;
+      pixq = st.pixq;
+      if (st.pc_ && B.r[st.q_cp].ok[F]) {
+        x[0] = E;
+        ce[0] = swapc(B.r[st.q_cp].c[F]);
+        for (int j = 1; j <= m; ++j) { x[j] = P.v[m + 1 - j]; ce[j] = swapc(P.ex[m + 1 - j]); }
+        x[m + 1] = P.v[0];
+        vp = path_value(S, x, ce, m + 2, F, A.mask);
+      }
+      if (qc_ && B.r[st.q_cq].ok[Fb]) {
+        x[0] = E;
+        ce[0] = swapc(B.r[st.q_cq].c[Fb]);
+        for (int j = 1; j <= m; ++j) { x[j] = Q.v[m + 1 - j]; ce[j] = swapc(Q.ex[m + 1 - j]); }
+        x[m + 1] = Q.v[0];
+        vq = path_value(S, x, ce, m + 2, Fb, A.mask);
       }
     }
-    if (hasP && !gotP) Pend = true;
-    if (A.reconnect && recon == 0 && qActive && hasP && div_m && rough_enough(mp, A.alpha_min) &&
-        rough_enough(mq, A.alpha_min)) {
-      // reconnection at w = m to the base vertex v_{m+1}
-      w = m;
-      if (!gotP) {
-        recon = 2;
-        reject_from = m + 1;
-        reject_reason = RJ_TARGET;
+    const int kind = Lroot ? 2 : 1;
+    if (st.pc_) {
+      int stt = ST_ACCEPTED, rs = RJ_NONE;
+      float R = 1.0f;
+      if (st.recon == 2 && m >= st.w + 1) { stt = ST_REJECTED; rs = st.reject_reason; }
+      else if (reconnected_here && m >= st.reject_from) { stt = ST_REJECTED; rs = st.reject_reason; }
+      else if (!qc_) stt = ST_UNPAIRED;
+      else if (reconnected_here) {
+        R = st.R1 * (m >= st.w + 2 ? st.R2 : 1.0f);
+        if (!(R > 0.0f) || !isfinite(R)) { stt = ST_REJECTED; rs = RJ_TARGET; }
+      }
+      if (stt == ST_ACCEPTED && A.reject_multi && st.hdiv && (st.dynP >= 2 || st.dynQ >= 2)) { stt = ST_REJECTED; rs = RJ_MULTI; }
+      finish(o, i, kind, m, 0, stt, rs, pixp, vp, pixq, vq, R);
+    } else if (qc_ && !A.two_way) {
+      finish(o, i, kind, m, 0, ST_MAPPED_ONLY, RJ_NONE, -1, f3(0.f, 0.f, 0.f), pixq, vq, 1.0f);
+    }
+  }
+  if (m >= maxW) return false;
+  // ---- walk results
+  bool gotP = false;
+  if (st.okP) {
+    const QRes& r = B.r[st.q_wp];
+    if (r.ok[F]) {
+      P.v[m + 1] = hit_pv(S, r.h[F], P.v[m].p, st.woP, F);
+      P.ex[m + 1] = r.c[F];
+      P.n = m + 1;
+      gotP = true;
+    }
+    if (st.walk_shared) {
+      if (r.ok[Fb]) {
+        Q.v[m + 1] = hit_pv(S, r.h[Fb], Q.v[m].p, st.woQ, Fb);
+        Q.ex[m + 1] = r.c[Fb];
+        Q.n = m + 1;
       } else {
-        const PV& vw = P.v[m];
-        const PV& vq = Q.v[m];
-        const PV& tg = P.v[m + 1];
-        float3 a = vq.p - tg.p, b = vw.p - tg.p;
-        float la2 = dot3(a, a), lb2 = dot3(b, b);
-        int rs = RJ_NONE;
-        Seg2 s;
-        if (edited(S, tg.obj)) rs = RJ_TARGET;                                              // (1) P:L406
-        else if (!rough_enough(load_mat(S, (uint32_t)tg.obj, F), A.alpha_min)) rs = RJ_TARGET;  // (2) P:L408
-        else if (fminf(sqrtf(lb2), sqrtf(la2)) < A.dmin) rs = RJ_TARGET;                   // (3) P:L410
-        else {
-          s = seg2(S, vq.p, tg.p, vq.tri, tg.tri, Fb == 0, Fb == 1, o.qc);
-          if (!s.vis[Fb]) rs = RJ_OCCLUDED;
-          else {
-            float Jg = fabsf(dot3(tg.n, a * (1.0f / sqrtf(la2)))) / fabsf(dot3(tg.n, b * (1.0f / sqrtf(lb2)))) * lb2 / la2;
-            if (!(Jg <= A.jacobian_max && Jg >= 1.0f / A.jacobian_max)) rs = RJ_JACOBIAN;
-          }
-        }
-        if (rs == RJ_NONE) {
-          R1 = area_pdf(S, Fb, Q.v[m - 1], vq, tg) / area_pdf(S, F, P.v[m - 1], vw, tg);
-          recon = 1;
-          Q.v[m + 1] = tg;
-          Q.ex[m + 1] = s.c[Fb];
-          Q.n = m + 1;
-        } else {
-          recon = 2;
-          reject_from = m + 1;
-          reject_reason = rs;
-        }
-      }
-    } else if (qActive && !shared) {
-      if (okQ) {
-        Trace2 t = trace2(S, Q.v[m].p, woQ, Q.v[m].tri, Fb == 0, Fb == 1, o.qc);
-        if (t.ok[Fb]) { Q.v[m + 1] = t.v[Fb]; Q.ex[m + 1] = t.c[Fb]; Q.n = m + 1; }
-        else Qend = true;
-      } else {
-        Qend = true;
-      }
-    } else if (recon == 1 && m >= w + 1 && gotP) {
-      // shared suffix edge v_m -> v_{m+1}, re-checked against dyn_Fbar only (instance query), with the
-      // Fbar ghost crossings for the mapped path's MIS
-      const PV& a = P.v[m];
-      const PV& b = P.v[m + 1];
-      float3 dv = b.p - a.p;
-      float L = sqrtf(dot3(dv, dv));
-      float3 dir = dv * (1.0f / L);
-      bool occ = occluded_dyn(S, Fb, a.p, dir, S.eps, L - S.eps, a.tri, b.tri);
-      Cross c = S.n_moved > 0 ? crossings(S, Fb, a.p, dir, S.eps, L - S.eps, L) : cross_zero();
-      o.qc.inst++;
-      if (occ && m + 1 < reject_from) { reject_from = m + 1; reject_reason = RJ_OCCLUDED; }
-      if (edited(S, b.obj) && m + 1 < reject_from) { reject_from = m + 1; reject_reason = RJ_SUFFIX_DYN; }
-      Q.v[m + 1] = b;
-      Q.ex[m + 1] = c;
-      Q.n = m + 1;
-      if (m == w + 1) {
-        R2 = area_pdf(S, Fb, Q.v[w], a, b) / area_pdf(S, F, P.v[w], a, b);
+        st.Qend = true;
       }
     }
-    rdiv = div_m;
-    if (recon == 1 && m >= w + 1 && !gotP) break;
-    if (Pend && (A.two_way || Qend || recon != 0)) break;
+  }
+  if (hasP && !gotP) st.Pend = true;
+  if (st.attempt) {
+    // reconnection at w = m to the base vertex v_{m+1}
+    st.w = m;
+    if (!gotP) {
+      st.recon = 2;
+      st.reject_from = m + 1;
+      st.reject_reason = RJ_TARGET;
+    } else {
+      const PV& vw = P.v[m];
+      const PV& vq = Q.v[m];
+      const PV& tg = P.v[m + 1];
+      float3 a = vq.p - tg.p, b = vw.p - tg.p;
+      float la2 = dot3(a, a), lb2 = dot3(b, b);
+      int rs = RJ_NONE;
+      if (edited(S, tg.obj)) rs = RJ_TARGET;                                                // (1) P:L406
+      else if (!rough_enough(load_mat(S, (uint32_t)tg.obj, F), A.alpha_min)) rs = RJ_TARGET;  // (2) P:L408
+      else if (fminf(sqrtf(lb2), sqrtf(la2)) < A.dmin) rs = RJ_TARGET;                     // (3) P:L410
+      else {
+        float Jg = fabsf(dot3(tg.n, a * (1.0f / sqrtf(la2)))) / fabsf(dot3(tg.n, b * (1.0f / sqrtf(lb2)))) * lb2 / la2;
+        if (!(Jg <= A.jacobian_max && Jg >= 1.0f / A.jacobian_max)) rs = RJ_JACOBIAN;
+      }
+      if (rs == RJ_NONE) {
+        st.R1 = area_pdf(S, Fb, Q.v[m - 1], vq, tg) / area_pdf(S, F, P.v[m - 1], vw, tg);
+        st.recon = 3;  // visibility of v'_w -> v_{w+1} in View_Fbar is checked with the next batch
+        Q.v[m + 1] = tg;
+        Q.n = m + 1;
+      } else {
+        st.recon = 2;
+        st.reject_from = m + 1;
+        st.reject_reason = rs;
+      }
+    }
+  } else if (st.qActive && !st.walk_shared) {
+    if (st.okQ) {
+      const QRes& r = B.r[st.q_wq];
+      if (r.ok[Fb]) {
+        Q.v[m + 1] = hit_pv(S, r.h[Fb], Q.v[m].p, st.woQ, Fb);
+        Q.ex[m + 1] = r.c[Fb];
+        Q.n = m + 1;
+      } else {
+        st.Qend = true;
+      }
+    } else {
+      st.Qend = true;
+    }
+  } else if (st.recon == 1 && m >= st.w + 1 && gotP) {
+    const PV& a = P.v[m];
+    const PV& b = P.v[m + 1];
+    st.suffix_pending = true;
+    if (edited(S, b.obj) && m + 1 < st.reject_from) { st.reject_from = m + 1; st.reject_reason = RJ_SUFFIX_DYN; }
+    Q.v[m + 1] = b;
+    Q.n = m + 1;
+    if (m == st.w + 1) st.R2 = area_pdf(S, Fb, Q.v[st.w], a, b) / area_pdf(S, F, P.v[st.w], a, b);
+  }
+  st.rdiv = st.div_m;
+  if (st.recon == 1 && m >= st.w + 1 && !gotP) return false;
+  if (st.Pend && (A.two_way || st.Qend || st.recon != 0)) return false;
+  int mn = m + 1;
+  bool hasP2 = mn <= P.n, hasQ2 = mn <= Q.n;
+  if (!hasP2 && (A.two_way || !hasQ2)) return false;
+  return true;
+}
+
+// advance one single-walk sample: consume the last batch (if any), issue the next; false when done
+__device__ bool single_step(const DevScene& S, const KArgs& A, SState& st, Batch& B, Out& o) {
+  const int F = A.side, Fb = 1 - F;
+  while (true) {
+    if (st.pc == 0) {
+      float d0[8];
+      st.rng.dims(0, d0);
+      B.n = 0;
+      if (A.tech == 7) {  // same pixel and jitter in both states: one trace serves both (A3)
+        int npix = S.W * S.H;
+        int pix = (int)(st.i % (uint64_t)npix);
+        st.sp.dir = camera_dir(S, (float)(pix % S.W) + d0[0], (float)(pix / S.W) + d0[1]);
+        st.sp.pix = st.sq.pix = pix;
+        st.sp.qi = st.sq.qi = B.push(mk_ray(S.cam_pos, st.sp.dir, -1, 3));
+      } else {
+        start_issue(S, A.tech, F, d0, st.sp, B);
+        start_issue(S, A.tech_q, Fb, d0, st.sq, B);
+      }
+      st.pc = 1;
+      if (B.n > 0) return true;
+      continue;
+    }
+    if (st.pc == 1) {
+      if (A.tech == 7) {
+        PV E = cam_pv(S);
+        st.P.n = st.Q.n = 0;
+        st.P.pixel = st.Q.pixel = st.sp.pix;
+        const QRes& r = B.r[st.sp.qi];
+        if (r.ok[F]) { st.P.v[0] = E; st.P.v[1] = hit_pv(S, r.h[F], E.p, st.sp.dir, F); st.P.ex[1] = r.c[F]; st.P.n = 1; }
+        if (r.ok[Fb]) { st.Q.v[0] = E; st.Q.v[1] = hit_pv(S, r.h[Fb], E.p, st.sp.dir, Fb); st.Q.ex[1] = r.c[Fb]; st.Q.n = 1; }
+      } else {
+        start_consume(S, A.tech, F, st.sp, B, st.P);
+        start_consume(S, A.tech_q, Fb, st.sq, B, st.Q);
+      }
+      if (st.P.n == 0 && (A.two_way || st.Q.n == 0)) return false;
+      st.m = 1;
+      st.recon = 0;
+      st.w = 0;
+      st.reject_from = 1 << 30;
+      st.reject_reason = RJ_NONE;
+      st.R1 = st.R2 = 1.0f;
+      st.rdiv = st.hdiv = st.suffix_pending = false;
+      st.dynP = st.dynQ = 0;
+      st.Pend = st.P.n == 0;
+      st.Qend = st.Q.n == 0;
+      st.pc = 2;
+      B.n = 0;
+      single_issue(S, A, st, B);
+      if (B.n > 0) return true;
+      continue;
+    }
+    if (!single_consume(S, A, st, B, o)) return false;
+    st.m++;
+    B.n = 0;
+    single_issue(S, A, st, B);
+    if (B.n > 0) return true;
   }
 }
 
 // ------------------------------------------------------------------------------------------------
 // two-ended techniques T3 / T6: pure replay
 // ------------------------------------------------------------------------------------------------
-struct Side {  // one sub-walk with its per-vertex connection
-  PV v[RR_MAXV - 2];
-  Cross ex[RR_MAXV - 2];
-  Cross cc[RR_MAXV - 2];  // connection-edge crossings (sensor: from v toward E; NEE: from v toward L)
-  PV L[RR_MAXV - 2];      // NEE vertex (emitter side)
-  int pix[RR_MAXV - 2];   // sensor pixel (sensor side), -1 if none
-  uint8_t vis[RR_MAXV - 2];
-  int n;
+#define BMAX (RR_MAXD - 2)
+struct BSide {  // one sub-walk with its per-vertex connection
+  PV v[BMAX + 1];
+  Cross ex[BMAX + 1];
+  Cross cc[BMAX + 1];  // connection-edge crossings (sensor: from v toward E; NEE: from v toward L)
+  PV L[BMAX + 1];      // NEE vertex (emitter side)
+  int pix[BMAX + 1];   // sensor pixel (sensor side)
+  uint8_t vis[BMAX + 1];
+  int n, nconn;        // walk vertices; vertices whose connection is done
+  bool ended;
+  int qw;              // query index of the pending walk step (-1 none)
+  int qc;              // query index of the pending connection (-1 none)
+  float3 wd;
 };
-struct Bidir {
+struct BPath {
   bool ok;
   PV start;
-  Side A, B;  // A: sensor side (slots t), B: emitter side (slots 16 + s)
+  float3 dir0, dir1;
+  int q0, q1, qyz;
+  BSide A, B;  // A: sensor side (slots t), B: emitter side (slots 16 + s)
+};
+struct BState {
+  uint64_t i;
+  Rng rng;
+  int pc, nmax;
+  BPath P, Q;
 };
 
-__device__ void extend_side(const DevScene& S, int F, const Rng& rng, Side& W, int slot0, int nmax, QCount& qc) {
-  while (W.n < nmax) {
-    int m = W.n;
-    float d[8];
-    rng.dims((uint32_t)(slot0 + m), d);
-    Mat mt = load_mat(S, (uint32_t)W.v[m].obj, F);
-    float3 wo;
-    if (!bsdf_sample(mt, W.v[m].n, norm3_exact(W.v[m - 1].p - W.v[m].p), d[1], d[2], wo)) break;
-    Trace2 t = trace2(S, W.v[m].p, wo, W.v[m].tri, F == 0, F == 1, qc);
-    if (!t.ok[F]) break;
-    W.v[m + 1] = t.v[F];
-    W.ex[m + 1] = t.c[F];
-    W.n = m + 1;
-  }
-}
-
-__device__ void gen_bidir(const DevScene& S, const KArgs& A, int tech, int F, const Rng& rng, Bidir& G, QCount& qc) {
+__device__ void bidir_start_issue(const DevScene& S, const KArgs& A, int tech, int F, const Rng& rng, BPath& G, Batch& B) {
   G.ok = false;
-  G.A.n = G.B.n = 0;
+  G.q0 = G.q1 = G.qyz = -1;
+  G.A.n = G.B.n = G.A.nconn = G.B.nconn = 0;
+  G.A.ended = G.B.ended = false;
+  G.A.qw = G.B.qw = G.A.qc = G.B.qc = -1;
   const int D = A.max_depth;
   float d0[8];
   rng.dims(0, d0);
-  int nmax;
   if (tech == 3) {
     if (S.n_edited == 0 || D < 4) return;
     PV xd = sample_set(S, S.edited_tris, S.edited_cdf, S.n_edited, F, d0[0], d0[1], d0[2]);
@@ -689,61 +523,111 @@ __device__ void gen_bidir(const DevScene& S, const KArgs& A, int tech, int F, co
     Mat mt = load_mat(S, (uint32_t)xd.obj, F);
     float3 we;
     if (!bsdf_sample(mt, xd.n, wl, d0[6], d0[7], we)) return;
-    Trace2 ty = trace2(S, xd.p, wl, xd.tri, F == 0, F == 1, qc);
-    if (!ty.ok[F]) return;
-    Trace2 tz = trace2(S, xd.p, we, xd.tri, F == 0, F == 1, qc);
-    if (!tz.ok[F]) return;
     G.start = xd;
-    G.B.v[0] = xd; G.B.v[1] = ty.v[F]; G.B.ex[1] = ty.c[F]; G.B.n = 1;
-    G.A.v[0] = xd; G.A.v[1] = tz.v[F]; G.A.ex[1] = tz.c[F]; G.A.n = 1;
-    nmax = D - 3;
+    G.dir0 = wl;
+    G.dir1 = we;
+    G.q0 = B.push(mk_ray(xd.p, wl, xd.tri, bit(F)));
+    G.q1 = B.push(mk_ray(xd.p, we, xd.tri, bit(F)));
   } else {
     if (S.n_moved == 0 || D < 3) return;
     PV xg = sample_set(S, S.moved_tris, S.moved_cdf, S.n_moved, 1 - F, d0[0], d0[1], d0[2]);
     float z = 1.0f - 2.0f * d0[3];
-    float rr = 2.0f * sqrtf(d0[3] * (1.0f - d0[3])), s, c;  // sqrt(1 - z^2) = 2 sqrt(u (1-u)), no cancellation
+    float rr = 2.0f * sqrtf(d0[3] * (1.0f - d0[3])), s, c;  // sqrt(1 - z^2), no cancellation
     sincosf(2.0f * RR_PI_F * d0[4], &s, &c);
     float3 dir = f3(rr * c, rr * s, z);
-    Trace2 ty = trace2(S, xg.p, dir, -1, F == 0, F == 1, qc);
-    if (!ty.ok[F]) return;
-    Trace2 tz = trace2(S, xg.p, dir * -1.0f, -1, F == 0, F == 1, qc);
-    if (!tz.ok[F]) return;
-    PV y1 = ty.v[F], z1 = tz.v[F];
-    // crossings of the whole edge (z_1, y_1), which passes through x_G
-    float3 dv = z1.p - y1.p;
-    float L = sqrtf(dot3(dv, dv));
-    Cross cyz = (S.n_moved > 0 && L > 2.0f * S.eps) ? crossings(S, F, y1.p, dv * (1.0f / L), S.eps, L - S.eps, L) : cross_zero();
-    qc.inst++;
     G.start = xg;
-    G.A.v[0] = y1; G.A.v[1] = z1; G.A.ex[1] = cyz; G.A.n = 1;
-    G.B.v[0] = z1; G.B.v[1] = y1; G.B.ex[1] = swapc(cyz); G.B.n = 1;
-    nmax = D - 2;
+    G.dir0 = dir;
+    G.dir1 = dir * -1.0f;
+    G.q0 = B.push(mk_ray(xg.p, dir, -1, bit(F)));
+    G.q1 = B.push(mk_ray(xg.p, G.dir1, -1, bit(F)));
   }
+}
+__device__ void bidir_start_consume(const DevScene& S, int tech, int F, BPath& G, const Batch& B) {
+  if (G.q0 < 0) return;
+  const QRes& ry = B.r[G.q0];
+  const QRes& rz = B.r[G.q1];
+  if (!ry.ok[F] || !rz.ok[F]) return;
+  PV y1 = hit_pv(S, ry.h[F], G.start.p, G.dir0, F);
+  PV z1 = hit_pv(S, rz.h[F], G.start.p, G.dir1, F);
   G.ok = true;
-  extend_side(S, F, rng, G.A, 0, nmax, qc);
-  extend_side(S, F, rng, G.B, 16, nmax, qc);
-  PV E = cam_pv(S);
-  for (int t = 1; t <= G.A.n; ++t) {  // sensor connections
-    const PV& z = G.A.v[t];
-    G.A.pix[t] = project(S, z.p);
-    Seg2 s = seg2(S, z.p, E.p, z.tri, -1, F == 0, F == 1, qc);
-    G.A.vis[t] = s.vis[F];
-    G.A.cc[t] = s.c[F];
+  if (tech == 3) {
+    G.B.v[0] = G.start; G.B.v[1] = y1; G.B.ex[1] = ry.c[F]; G.B.n = 1;
+    G.A.v[0] = G.start; G.A.v[1] = z1; G.A.ex[1] = rz.c[F]; G.A.n = 1;
+  } else {
+    G.A.v[0] = y1; G.A.v[1] = z1; G.A.n = 1;  // edge (z_1, y_1): crossings by a segment query next step
+    G.B.v[0] = z1; G.B.v[1] = y1; G.B.n = 1;
+    G.A.ex[1] = G.B.ex[1] = cross_zero();
   }
-  for (int sdx = 1; sdx <= G.B.n; ++sdx) {  // NEE, slot 16 + s
-    const PV& y = G.B.v[sdx];
-    float d[8];
-    rng.dims((uint32_t)(16 + sdx), d);
-    PV L = sample_emitter(S, d[3], d[4], d[5], d[6]);
-    G.B.L[sdx] = L;
-    Seg2 s = seg2(S, y.p, L.p, y.tri, L.tri, F == 0, F == 1, qc);
-    G.B.vis[sdx] = s.vis[F];
-    G.B.cc[sdx] = s.c[F];
+}
+// issue the next queries of one path: T6 edge crossings, pending connections, walk steps
+__device__ void bidir_issue(const DevScene& S, const KArgs& A, int tech, int F, const Rng& rng, int nmax, BPath& G,
+                            Batch& B, bool first) {
+  G.qyz = -1;
+  G.A.qw = G.B.qw = G.A.qc = G.B.qc = -1;
+  if (!G.ok) return;
+  if (first && tech == 6 && S.n_moved > 0) {
+    G.qyz = B.push(mk_seg(G.A.v[0].p, G.A.v[1].p, -2, -2, bit(F)));  // crossings of the whole edge
+  }
+  PV E = cam_pv(S);
+  for (int side = 0; side < 2; ++side) {
+    BSide& W = side == 0 ? G.A : G.B;
+    if (W.nconn < W.n) {  // connection of the newest vertex
+      int t = W.nconn + 1;
+      const PV& v = W.v[t];
+      if (side == 0) {
+        W.pix[t] = project(S, v.p);
+        W.qc = B.push(mk_seg(v.p, E.p, v.tri, -1, bit(F)));
+      } else {
+        float d[8];
+        rng.dims((uint32_t)(16 + t), d);
+        W.L[t] = sample_emitter(S, d[3], d[4], d[5], d[6]);
+        W.qc = B.push(mk_seg(v.p, W.L[t].p, v.tri, W.L[t].tri, bit(F)));
+      }
+    }
+    if (!W.ended && W.n < nmax) {
+      int m = W.n;
+      float d[8];
+      rng.dims((uint32_t)((side == 0 ? 0 : 16) + m), d);
+      Mat mt = load_mat(S, (uint32_t)W.v[m].obj, F);
+      if (bsdf_sample(mt, W.v[m].n, norm3_exact(W.v[m - 1].p - W.v[m].p), d[1], d[2], W.wd))
+        W.qw = B.push(mk_ray(W.v[m].p, W.wd, W.v[m].tri, bit(F)));
+      else
+        W.ended = true;
+    } else {
+      W.ended = true;
+    }
+  }
+}
+__device__ void bidir_consume(const DevScene& S, int F, BPath& G, const Batch& B) {
+  if (!G.ok) return;
+  if (G.qyz >= 0) {
+    G.A.ex[1] = B.r[G.qyz].c[F];
+    G.B.ex[1] = swapc(G.A.ex[1]);
+  }
+  for (int side = 0; side < 2; ++side) {
+    BSide& W = side == 0 ? G.A : G.B;
+    if (W.qc >= 0) {
+      int t = W.nconn + 1;
+      W.vis[t] = B.r[W.qc].ok[F];
+      W.cc[t] = B.r[W.qc].c[F];
+      W.nconn = t;
+    }
+    if (W.qw >= 0) {
+      const QRes& r = B.r[W.qw];
+      if (r.ok[F]) {
+        int m = W.n;
+        W.v[m + 1] = hit_pv(S, r.h[F], W.v[m].p, W.wd, F);
+        W.ex[m + 1] = r.c[F];
+        W.n = m + 1;
+      } else {
+        W.ended = true;
+      }
+    }
   }
 }
 
 // path (E, z_t..z_1, [x_D], y_1..y_s, L) of a two-ended sample
-__device__ int bidir_path(const Bidir& G, int tech, int t, int s, const DevScene& S, PV* x, Cross* ce) {
+__device__ int bidir_path(const BPath& G, int tech, int t, int s, const DevScene& S, PV* x, Cross* ce) {
   int k = 0;
   x[k] = cam_pv(S);
   ce[k] = swapc(G.A.cc[t]);
@@ -771,18 +655,13 @@ __device__ int bidir_path(const Bidir& G, int tech, int t, int s, const DevScene
   return k;
 }
 
-__device__ void sample_bidir(const DevScene& S, const KArgs& A, uint64_t i, const Rng& rng, Out& o) {
-  const int F = A.side, Fb = 1 - A.side;
-  const int l = A.tech;
-  Bidir P, Q;
-  gen_bidir(S, A, l, F, rng, P, o.qc);
-  gen_bidir(S, A, l, Fb, rng, Q, o.qc);
-  if (!P.ok && (A.two_way || !Q.ok)) return;
+__device__ void bidir_finish(const DevScene& S, const KArgs& A, BState& st, Out& o) {
+  const int F = A.side, Fb = 1 - A.side, l = A.tech, D = A.max_depth;
+  BPath& P = st.P;
+  BPath& Q = st.Q;
   const int extra = (l == 3) ? 2 : 1;
-  const int D = A.max_depth;
   PV x[RR_MAXV + 2];
   Cross ce[RR_MAXV + 2];
-  // divergence / dynamic-vertex prefix data per side
   bool sdiff = P.ok && Q.ok && (l == 3) && !same_pv(S, P.start, Q.start);
   int nA = P.ok ? P.A.n : 0, nB = P.ok ? P.B.n : 0;
   int mA = Q.ok ? Q.A.n : 0, mB = Q.ok ? Q.B.n : 0;
@@ -810,8 +689,8 @@ __device__ void sample_bidir(const DevScene& S, const KArgs& A, uint64_t i, cons
         }
       }
       if (pc) {
-        int st = qc_ ? ST_ACCEPTED : ST_UNPAIRED, rs = RJ_NONE;
-        if (st == ST_ACCEPTED && A.reject_multi) {
+        int stt = qc_ ? ST_ACCEPTED : ST_UNPAIRED, rs = RJ_NONE;
+        if (stt == ST_ACCEPTED && A.reject_multi) {
           bool dv = sdiff;
           int dp = (l == 3) ? 1 : 0, dq = dp;
           for (int j = (l == 3 ? 1 : 0); j <= t; ++j) {
@@ -823,68 +702,158 @@ __device__ void sample_bidir(const DevScene& S, const KArgs& A, uint64_t i, cons
             dp += edited(S, P.B.v[j].obj);
             dq += edited(S, Q.B.v[j].obj);
           }
-          if (dv && (dp >= 2 || dq >= 2)) { st = ST_REJECTED; rs = RJ_MULTI; }
+          if (dv && (dp >= 2 || dq >= 2)) { stt = ST_REJECTED; rs = RJ_MULTI; }
         }
-        finish(o, i, 3, t, s, st, rs, pixp, vp, pixq, vq, 1.0f);
+        finish(o, st.i, 3, t, s, stt, rs, pixp, vp, pixq, vq, 1.0f);
       } else {
-        finish(o, i, 3, t, s, ST_MAPPED_ONLY, RJ_NONE, -1, f3(0.f, 0.f, 0.f), pixq, vq, 1.0f);
+        finish(o, st.i, 3, t, s, ST_MAPPED_ONLY, RJ_NONE, -1, f3(0.f, 0.f, 0.f), pixq, vq, 1.0f);
       }
     }
   }
 }
 
+__device__ bool bidir_step(const DevScene& S, const KArgs& A, BState& st, Batch& B, Out& o) {
+  const int F = A.side, Fb = 1 - F, l = A.tech;
+  while (true) {
+    if (st.pc == 0) {
+      B.n = 0;
+      st.nmax = l == 3 ? A.max_depth - 3 : A.max_depth - 2;
+      bidir_start_issue(S, A, l, F, st.rng, st.P, B);
+      bidir_start_issue(S, A, l, Fb, st.rng, st.Q, B);
+      st.pc = 1;
+      if (B.n > 0) return true;
+      continue;
+    }
+    if (st.pc == 1) {
+      bidir_start_consume(S, l, F, st.P, B);
+      bidir_start_consume(S, l, Fb, st.Q, B);
+      if (!st.P.ok && (A.two_way || !st.Q.ok)) return false;
+      B.n = 0;
+      bidir_issue(S, A, l, F, st.rng, st.nmax, st.P, B, true);
+      bidir_issue(S, A, l, Fb, st.rng, st.nmax, st.Q, B, true);
+      st.pc = 2;
+      if (B.n > 0) return true;
+      continue;
+    }
+    bidir_consume(S, F, st.P, B);
+    bidir_consume(S, Fb, st.Q, B);
+    B.n = 0;
+    bidir_issue(S, A, l, F, st.rng, st.nmax, st.P, B, false);
+    bidir_issue(S, A, l, Fb, st.rng, st.nmax, st.Q, B, false);
+    if (B.n > 0) return true;
+    bidir_finish(S, A, st, o);
+    return false;
+  }
+}
+
 // ------------------------------------------------------------------------------------------------
-// kernel: grid-stride over this shard's samples of one (technique, side)
+// kernel: persistent lanes over this shard's samples of one (technique, side)
 // ------------------------------------------------------------------------------------------------
 __device__ __forceinline__ void warp_add(unsigned long long* p, uint32_t v) {
-  uint32_t s = __reduce_add_sync(0xffffffffu, v);
+  uint32_t s = __reduce_add_sync(FULLMASK, v);
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(p, (unsigned long long)s);
 }
 
-__global__ void __launch_bounds__(128) k_residual(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
+// warp-aggregated fetch of the next local sample slot for every lane in `need`
+__device__ __forceinline__ uint64_t fetch_work(unsigned long long* counter, bool need) {
+  unsigned m = __ballot_sync(FULLMASK, need);
+  unsigned long long base = 0;
+  int lane = threadIdx.x & 31;
+  if (m) {
+    int leader = __ffs(m) - 1;
+    if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(m));
+    base = __shfl_sync(FULLMASK, base, leader);
+  }
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
+template <class State, bool BIDIR>
+__device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A) {
   Out o;
   o.A = &A;
   o.qc.closest = o.qc.shadow = o.qc.inst = 0;
+  o.qc.tc.nodes = o.qc.tc.tris = 0;
   o.conns = o.acc = o.rej = o.unp = o.monly = o.recon = o.splats = o.offscreen = o.zero = 0;
   for (int r = 0; r < 6; ++r) o.rejby[r] = 0;
   uint32_t nsamp = 0;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t base = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  // all lanes iterate the same number of times (warp-synchronous reductions at the end)
-  for (uint64_t li = base; li - threadIdx.x % 32 < A.n_local; li += stride) {
-    if (li >= A.n_local) continue;
-    uint64_t i;
-    if (A.dump) {
-      i = A.i_begin + li;
-    } else {
-      uint64_t blk = li >> 16, off = li & 0xFFFFull;
-      i = ((blk * A.shard_count + A.shard_index) << 16) | off;
-      if (i >= A.n_total) continue;
+  State st;
+  Batch B;
+  bool active = false, more = true;
+  while (true) {
+    // refill: lanes without a sample take the next local slot (warp-aggregated atomics)
+    if (!active) B.n = 0;
+    while (true) {
+      bool need = !active && more;
+      if (!__any_sync(FULLMASK, need)) break;
+      uint64_t li = fetch_work(A.work, need);
+      if (need) {
+        if (li >= A.n_local) {
+          more = false;
+        } else {
+          uint64_t i;
+          bool valid = true;
+          if (A.dump) {
+            i = A.i_begin + li;
+          } else {
+            uint64_t blk = li >> 16, off = li & 0xFFFFull;
+            i = ((blk * A.shard_count + A.shard_index) << 16) | off;
+            valid = i < A.n_total;
+          }
+          if (valid) {
+            nsamp++;
+            st.i = i;
+            st.rng.i_lo = (uint32_t)i;
+            st.rng.i_hi = (uint32_t)(i >> 32);
+            st.rng.ls = (uint32_t)A.tech | ((uint32_t)A.side << 8);
+            st.rng.k0 = (uint32_t)A.seed;
+            st.rng.k1 = (uint32_t)(A.seed >> 32);
+            st.pc = 0;
+            bool go;
+            if constexpr (BIDIR) go = bidir_step(S, A, st, B, o);
+            else go = single_step(S, A, st, B, o);
+            active = go;
+            if (!go) B.n = 0;
+          }
+        }
+      }
     }
-    Rng rng;
-    rng.i_lo = (uint32_t)i;
-    rng.i_hi = (uint32_t)(i >> 32);
-    rng.ls = (uint32_t)A.tech | ((uint32_t)A.side << 8);
-    rng.k0 = (uint32_t)A.seed;
-    rng.k1 = (uint32_t)(A.seed >> 32);
-    nsamp++;
-    if (A.tech == 3 || A.tech == 6) sample_bidir(S, A, i, rng, o);
-    else sample_single(S, A, i, rng, o);
+    int nmax = (int)__reduce_max_sync(FULLMASK, (unsigned)B.n);
+    if (nmax == 0 && !__any_sync(FULLMASK, active || more)) break;
+    // all queries of the warp through the single traversal site
+    for (int k = 0; k < nmax; ++k)
+      if (k < B.n) run_query(S, B.q[k], B.r[k], o.qc);
+    if (active) {
+      bool go;
+      if constexpr (BIDIR) go = bidir_step(S, A, st, B, o);
+      else go = single_step(S, A, st, B, o);
+      active = go;
+      if (!active) B.n = 0;
+    }
   }
-  unsigned long long* st = A.stats;
-  warp_add(st + STAT_SAMPLES, nsamp);
-  warp_add(st + STAT_CONNECTIONS, o.conns);
-  warp_add(st + STAT_ACCEPTED, o.acc);
-  warp_add(st + STAT_REJECTED, o.rej);
-  warp_add(st + STAT_UNPAIRED, o.unp);
-  warp_add(st + STAT_MAPPED_ONLY, o.monly);
-  warp_add(st + STAT_CLOSEST, o.qc.closest);
-  warp_add(st + STAT_SHADOW, o.qc.shadow);
-  warp_add(st + STAT_INST, o.qc.inst);
-  warp_add(st + STAT_SPLATS, o.splats);
-  warp_add(st + STAT_OFFSCREEN, o.offscreen);
-  warp_add(st + STAT_ZERO, o.zero);
-  for (int r = 0; r < 6; ++r) warp_add(st + STAT_REJBY + r, o.rejby[r]);
+  unsigned long long* stt = A.stats;
+  warp_add(stt + STAT_SAMPLES, nsamp);
+  warp_add(stt + STAT_CONNECTIONS, o.conns);
+  warp_add(stt + STAT_ACCEPTED, o.acc);
+  warp_add(stt + STAT_REJECTED, o.rej);
+  warp_add(stt + STAT_UNPAIRED, o.unp);
+  warp_add(stt + STAT_MAPPED_ONLY, o.monly);
+  warp_add(stt + STAT_RECONNECTED, o.recon);
+  warp_add(stt + STAT_CLOSEST, o.qc.closest);
+  warp_add(stt + STAT_SHADOW, o.qc.shadow);
+  warp_add(stt + STAT_INST, o.qc.inst);
+  warp_add(stt + STAT_NODES, o.qc.tc.nodes);
+  warp_add(stt + STAT_TRIS, o.qc.tc.tris);
+  warp_add(stt + STAT_SPLATS, o.splats);
+  warp_add(stt + STAT_OFFSCREEN, o.offscreen);
+  warp_add(stt + STAT_ZERO, o.zero);
+  for (int r = 0; r < 6; ++r) warp_add(stt + STAT_REJBY + r, o.rejby[r]);
+}
+
+__global__ void __launch_bounds__(128) k_residual_single(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
+  residual_loop<SState, false>(S, A);
+}
+__global__ void __launch_bounds__(128) k_residual_bidir(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
+  residual_loop<BState, true>(S, A);
 }
 
 __global__ void k_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out) {
@@ -902,14 +871,15 @@ __global__ void k_trace(const __grid_constant__ DevScene S, int F, uint32_t n, c
   float3 o = f3(r[0], r[1], r[2]);
   float3 d = norm3_exact(f3(r[3], r[4], r[5]));
   int excl = __float_as_int(r[6]);
-  QCount qc;
-  Trace2 tr = trace2(S, o, d, excl, F == 0, F == 1, qc);
+  QCount qc = {};
+  QRes res;
+  run_query(S, mk_ray(o, d, excl, bit(F)), res, qc);
   float* h = hits + 8 * t;
-  if (!tr.ok[F]) {
+  if (!res.ok[F]) {
     h[0] = -1.0f;
     return;
   }
-  const PV& v = tr.v[F];
+  PV v = hit_pv(S, res.h[F], o, d, F);
   float3 q = v.p - o;
   h[0] = sqrtf(dot3(q, q));
   h[1] = __int_as_float(v.tri);
@@ -921,11 +891,12 @@ __global__ void k_segment(const __grid_constant__ DevScene S, uint32_t n, const 
   uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const float* s = segs + 6 * t;
-  QCount qc;
-  Seg2 r = seg2(S, f3(s[0], s[1], s[2]), f3(s[3], s[4], s[5]), -1, -1, true, true, qc);
+  QCount qc = {};
+  QRes r;
+  run_query(S, mk_seg(f3(s[0], s[1], s[2]), f3(s[3], s[4], s[5]), -1, -1, 3), r, qc);
   float* o = out + 10 * t;
   for (int F = 0; F < 2; ++F) {
-    o[5 * F] = r.vis[F] ? 1.0f : 0.0f;
+    o[5 * F] = r.ok[F] ? 1.0f : 0.0f;
     o[5 * F + 1] = r.c[F].n;
     o[5 * F + 2] = r.c[F].s0;
     o[5 * F + 3] = r.c[F].sa;
@@ -935,7 +906,8 @@ __global__ void k_segment(const __grid_constant__ DevScene S, uint32_t n, const 
 
 // ---- host launchers
 void launch_residual(const DevScene& S, const KArgs& A, int grid, cudaStream_t st) {
-  k_residual<<<grid, 128, 0, st>>>(S, A);
+  if (A.tech == 3 || A.tech == 6) k_residual_bidir<<<grid, 128, 0, st>>>(S, A);
+  else k_residual_single<<<grid, 128, 0, st>>>(S, A);
 }
 void launch_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out, cudaStream_t st) {
   k_philox<<<(n + 255) / 256, 256, 0, st>>>(n, ctr, k0, k1, out);

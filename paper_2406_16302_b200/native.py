@@ -51,7 +51,8 @@ class rr_render_args(C.Structure):
 class rr_stats(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("samples", "connections", "accepted", "rejected", "unpaired",
                                           "mapped_only", "reconnected", "closest_rays", "shadow_rays",
-                                          "instance_queries", "splats", "offscreen", "zero_pairs")] + \
+                                          "instance_queries", "splats", "offscreen", "zero_pairs",
+                                          "nodes_visited", "tris_tested")] + \
                [("rejected_by", C.c_uint64 * 8), ("effective_mask", C.c_uint32), ("n_moved", C.c_uint32)]
 
     def as_dict(self):
