@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""Benchmark: residual samples/s (and Mrays/s) of the B200 residual path integral renderer.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+One step = one complete rr_render_residual of the workload (every enabled technique, both sides of the
+two-way estimator) over this rank's sample shard, followed for N > 1 by the single NCCL
+reduce of the residual image.  Inputs (scene + LBVH) are resident in HBM when the timed region
+starts; the BVH (~350 MB for config 4) is larger than the 126 MB L2, so no flush is needed.  Rank 0 prints
+ONE JSON line.  Under torchrun (N > 1) every rank renders its block-cyclic shard of sample indices.
+
+--impl reference times the CPU oracle (oracle/, single-threaded fp64 C++) on the host cores on a bounded
+sample of the same workload; it is the reference arm of the driver's comparison, not the target.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from rr_inputs import scenes as S  # noqa: E402
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", type=int, default=4)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=1)
+    return p.parse_args()
+
+
+def workload(cfg: int):
+    return S.load_config(cfg)
+
+
+def techniques_in(w) -> int:
+    mask = w.args.technique_mask
+    moved = any(not np.array_equal(e.old_xform, e.new_xform) for e in w.edits)
+    if not moved:
+        mask &= ~0x38
+    return bin(mask).count("1")
+
+
+def samples_per_render(w) -> int:
+    c = w.scene.camera
+    return techniques_in(w) * c.width * c.height * w.args.spp
+
+
+# ---------------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.gpu), "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+
+        def rd():
+            for line in self.proc.stdout:
+                self.rows.append([x.strip() for x in line.split(",")])
+        self.thread = threading.Thread(target=rd, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+                for n, v in zip(names, r[4:8]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------- oracle
+_ORACLE = None
+
+
+def _oracle_worker(job):
+    l, side, i0, i1 = job
+    t = time.perf_counter()
+    _, _, st = _ORACLE.residual(_ARGS, l, side, i0, i1)
+    return time.perf_counter() - t, i1 - i0, st["closest_rays"] + st["shadow_rays"]
+
+
+def oracle_time(w, per_tech: int, cores: int):
+    """Time the oracle (as it stands) on the first `per_tech` indices of every (technique, side), split
+    over `cores` forked worker processes (counter-based RNG: disjoint index ranges are exact)."""
+    global _ORACLE, _ARGS
+    import multiprocessing as mp
+    from oracle import binding as OB
+    _ORACLE = OB.Oracle(w.scene, w.edits)
+    _ARGS = w.args
+    mask = _ORACLE.effective_mask(w.args.technique_mask)
+    jobs = []
+    chunk = max(1, per_tech // cores)
+    for l in range(1, 8):
+        if (mask >> (l - 1)) & 1:
+            for s in (0, 1):
+                for a in range(0, per_tech, chunk):
+                    jobs.append((l, s, a, min(per_tech, a + chunk)))
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(cores) as p:
+        res = p.map(_oracle_worker, jobs)
+    wall = time.perf_counter() - t0
+    n = sum(r[1] for r in res)
+    rays = sum(r[2] for r in res)
+    return n, rays, wall
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = workload(a.config)
+    cores = cpu_cores()
+    per_tech = 1024
+    c = w.scene.camera
+    vals = []
+    for k in range(a.warmup + a.steps):
+        n, rays, wall = oracle_time(w, per_tech, cores)
+        if k >= a.warmup:
+            vals.append((n, rays, wall))
+    n = sum(v[0] for v in vals)
+    wall = sum(v[2] for v in vals)
+    rays = sum(v[1] for v in vals)
+    value = n / wall
+    line = {
+        "impl": "reference", "metric": "residual_samples_per_s", "value": value, "unit": "samples/s",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * wall / max(1, a.steps),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "scene": w.scene.name, "resolution": [c.width, c.height], "spp": w.args.spp,
+                   "max_depth": w.args.max_depth, "sample": f"first {per_tech} indices of each (technique, side) per step"},
+        "mrays_per_s": rays / wall / 1e6,
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "oracle",
+                         "sample": f"first {per_tech} indices of each (technique, side), {a.steps} timed steps"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------- ours
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    from paper_2406_16302_b200 import Renderer, native
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    w = workload(a.config)
+    args = w.args
+    c = w.scene.camera
+    r = Renderer(local)
+    t0 = time.time()
+    r.upload(w.scene)
+    r.set_edit(w.edits)
+    torch.cuda.synchronize(dev)
+    upload_s = time.time() - t0
+    img = torch.empty((c.height, c.width, 4), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        r.render_residual(args, image=img, shard_index=rank, shard_count=world)
+        if world > 1:
+            dist.reduce(img, dst=0, op=dist.ReduceOp.SUM)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    # ---- timed region (device events on the render stream, max over ranks)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats_acc = {"closest_rays": 0, "shadow_rays": 0, "nodes_visited": 0, "tris_tested": 0, "samples": 0}
+    kern_ms = 0.0
+    launches = 0
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    # per-step counters and per-launch kernel times of the last step (same work every step)
+    st = r.get_stats()
+    tm = r.last_timings(16)
+    launch_ms = [x for x in tm[1:15] if x > 0]
+    launches = len(launch_ms)
+    kern_ms = sum(launch_ms)
+    for k in stats_acc:
+        stats_acc[k] = st[k]
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    cnt = torch.tensor([float(stats_acc[k]) for k in ("closest_rays", "shadow_rays", "nodes_visited", "tris_tested",
+                                                       "samples")], dtype=torch.float64, device=dev)
+    kt = torch.tensor([kern_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+        dist.all_reduce(kt, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    closest, shadow, nodes, tris, samples = [float(x) for x in cnt.tolist()]
+    total_samples = samples_per_render(w)
+    assert abs(samples - total_samples) < 0.5, (samples, total_samples)
+    value = total_samples * a.steps / (ms / 1e3)
+    mrays = (closest + shadow) * a.steps / (ms / 1e3) / 1e6
+    # ---- roofline of the dominant kernel family (the residual kernels: every launch of the step)
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        peaks = json.load(open(peaks_path))
+        hbm = float(peaks["hbm_gbs"])
+        peak_src = "measured"
+    except Exception:
+        hbm, peak_src = 6650.0, "fallback"
+    alg_bytes_step = 64.0 * nodes + 48.0 * tris  # BVH2 node (64 B) and triangle (48 B) fetches, SURVEY 8(d)
+    kms = float(kt.item())
+    achieved = alg_bytes_step / (kms / 1e3) / 1e9 if kms > 0 else None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": (achieved / hbm) if achieved else None, "traffic": None,
+                "kernel": "k_residual_single + k_residual_bidir (all launches of one render)",
+                "peak_source": peak_src, "algorithmic_bytes_per_step": alg_bytes_step,
+                "kernel_ms_per_step": kms}
+    prof = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(prof):
+        try:
+            roofline["traffic"] = json.load(open(prof)).get(f"config{a.config}")
+        except Exception:
+            pass
+    # ---- end to end through the public API with host buffers (one render per step)
+    e2e = None
+    if rank == 0 and world == 1:
+        host = np.zeros((c.height, c.width, 4), np.float32)
+        r.render_residual_host(args, out=host)  # warm
+        t1 = time.perf_counter()
+        for _ in range(a.e2e_steps):
+            r.set_edit(w.edits)                    # per-step inputs: the edit (host -> device)
+            r.render_residual_host(args, out=host)  # render + image copy device -> host
+        el = time.perf_counter() - t1
+        h2d = len(w.edits) * C_sizeof_edit() + C_sizeof_args()
+        e2e = {"value": total_samples * a.e2e_steps / el, "unit": "samples/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(host.nbytes)}
+    # ---- CPU baseline (oracle) on the host cores, rank 0 at N = 1 only
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cores = cpu_cores()
+        per_tech = 256
+        n, rays, wall = oracle_time(w, per_tech, cores)
+        cpu = {"value": n / wall, "unit": "samples/s", "cores": cores, "kind": "oracle",
+               "sample": f"first {per_tech} indices of each (technique, side) of {w.name}",
+               "mrays_per_s": rays / wall / 1e6}
+    if rank == 0:
+        line = {
+            "metric": "residual_samples_per_s", "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": w.name, "scene": w.scene.name, "triangles": w.scene.n_triangles,
+                       "resolution": [c.width, c.height], "spp": args.spp, "max_depth": args.max_depth,
+                       "techniques": techniques_in(w), "flags": "two_way+reconnect+reject_multi",
+                       "samples_per_step": total_samples, "parallelism": f"sample-shard x{world} + NCCL reduce",
+                       "l2": "inputs larger than L2 (BVH ~350 MB vs 126 MB L2)"},
+            "mrays_per_s": mrays,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches * a.steps,
+            "clocks": clk,
+            "upload_s": upload_s,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def C_sizeof_edit() -> int:
+    import ctypes
+    from paper_2406_16302_b200 import native
+    return ctypes.sizeof(native.rr_edit)
+
+
+def C_sizeof_args() -> int:
+    import ctypes
+    from paper_2406_16302_b200 import native
+    return ctypes.sizeof(native.rr_render_args)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
