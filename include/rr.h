@@ -127,6 +127,10 @@ typedef struct {
   uint64_t rejected_by[8]; /* by reason: 1 occluded, 2 jacobian, 3 multi, 4 target, 5 suffix-dynamic */
   uint32_t effective_mask; /* technique mask after auto-disable (T4-T6 off without moved objects) */
   uint32_t n_moved;        /* moved objects in the current edit */
+  uint64_t sched[8];       /* warp-scheduler occupancy of the residual kernels (diagnostics): [0] warp
+                              rounds, [1] lanes tracing summed over traversal slices, [2] sample steps,
+                              [3] queries per round summed, [4] lanes holding a sample summed over
+                              rounds, [5] traversal slices */
 } rr_stats;
 
 /* one record per emitted base connection (C10), for parity tests */

@@ -39,6 +39,8 @@ struct rr_ctx {
   DevBuf<int> d_obj_inst, obj_emitter, emit_off, emit_cnt;
   DevBuf<float> emit_pL, emit_cdf, edited_cdf, moved_cdf;
   DevBuf<unsigned long long> stats, work;
+  DevBuf<char> batch;   // per-lane query batches of the residual kernels (rr_residual.cu)
+  size_t batch_lanes = 0;
   DevScene S;
   uint32_t last_mask = 0;
   int edited_equals_moved = 0;
@@ -556,11 +558,19 @@ static KArgs make_kargs(rr_ctx* c, const rr_render_args* a, uint32_t mask, int l
   K.stats = c->stats.p;
   return K;
 }
-// persistent lanes: enough blocks to fill every SM (148 on B200) several times, fewer for tiny launches
-static int grid_for(uint64_t n) {
-  uint64_t g = (n + 127) / 128;
-  uint64_t cap = 148ull * 8;
-  return (int)std::max<uint64_t>(1, std::min(g, cap));
+// grid of one residual launch and its per-lane query batch buffers (grown on demand)
+static int prepare_launch(rr_ctx* c, KArgs& K) {
+  bool bidir = K.tech == 3 || K.tech == 6;
+  int grid = residual_grid(bidir, K.n_local);
+  size_t lanes = std::max((size_t)residual_grid(false, 1ull << 40), (size_t)residual_grid(true, 1ull << 40)) * residual_block();
+  if (c->batch_lanes < lanes) {
+    c->batch.alloc(lanes * batch_bytes_per_lane());
+    c->batch_lanes = lanes;
+  }
+  K.nlanes = grid * residual_block();
+  K.qbuf = reinterpret_cast<Query*>(c->batch.p);
+  K.rbuf = reinterpret_cast<QRes*>(c->batch.p + c->batch_lanes * query_slot_bytes());
+  return grid;
 }
 
 rr_status rr_render_residual(rr_ctx* c, const rr_render_args* a, float* d_image, uint64_t stream) {
@@ -592,7 +602,7 @@ rr_status rr_render_residual(rr_ctx* c, const rr_render_args* a, float* d_image,
       K.image = d_image;
       K.work = c->work.p + (nl++);
       if (K.n_local == 0) continue;
-      launch_residual(c->S, K, grid_for(K.n_local), st);
+      launch_residual(c->S, K, prepare_launch(c, K), st);
       if (ne < 16) cudaEventRecord(c->ev[ne++], st);
     }
   }
@@ -641,6 +651,7 @@ rr_status rr_get_stats(rr_ctx* c, rr_stats* out) {
   out->nodes_visited = h[STAT_NODES];
   out->tris_tested = h[STAT_TRIS];
   for (int r = 0; r < 6; ++r) out->rejected_by[r] = h[STAT_REJBY + r];
+  for (int r = 0; r < 8; ++r) out->sched[r] = h[STAT_SCHED + r];
   out->effective_mask = c->last_mask;
   out->n_moved = 0;
   for (int k = 0; k < c->S.n_inst; ++k) out->n_moved += c->S.inst[k].moved ? 1 : 0;
@@ -685,7 +696,7 @@ rr_status rr_dump_paths(rr_ctx* c, const rr_render_args* a, uint32_t technique, 
     K.recs = recs.p;
     K.rec_count = cnt.p;
     K.rec_cap = capacity;
-    launch_residual(c->S, K, grid_for(K.n_local), 0);
+    launch_residual(c->S, K, prepare_launch(c, K), 0);
     if (cudaDeviceSynchronize() != cudaSuccess) return cuda_check(c, "dump");
     unsigned long long n = 0;
     cudaMemcpy(&n, cnt.p, sizeof(n), cudaMemcpyDeviceToHost);

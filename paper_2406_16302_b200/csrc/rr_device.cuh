@@ -36,6 +36,22 @@ __device__ __forceinline__ bool eq3(float3 a, float3 b) {
   return __float_as_uint(a.x) == __float_as_uint(b.x) && __float_as_uint(a.y) == __float_as_uint(b.y) &&
          __float_as_uint(a.z) == __float_as_uint(b.z);
 }
+// Path-vertex positions are kept in fp64 (P3): a hit point is the exact intersection of the fp32 ray with
+// the triangle's plane, and the vector between two vertices is formed in fp64 before it is rounded, so a
+// short path edge keeps full fp32 relative precision in its direction and length.
+typedef double3 P3;
+__device__ __forceinline__ P3 p3(float3 a) { return make_double3(a.x, a.y, a.z); }
+__device__ __forceinline__ float3 f3of(P3 a) { return f3((float)a.x, (float)a.y, (float)a.z); }
+__device__ __forceinline__ float3 sub3(P3 a, P3 b) { return f3((float)(a.x - b.x), (float)(a.y - b.y), (float)(a.z - b.z)); }
+__device__ __forceinline__ bool eqp(P3 a, P3 b) {
+  return __double_as_longlong(a.x) == __double_as_longlong(b.x) && __double_as_longlong(a.y) == __double_as_longlong(b.y) &&
+         __double_as_longlong(a.z) == __double_as_longlong(b.z);
+}
+__device__ __forceinline__ P3 xf_point_d(const float* m, P3 p) {
+  return make_double3(fma((double)m[0], p.x, fma((double)m[1], p.y, fma((double)m[2], p.z, (double)m[3]))),
+                      fma((double)m[4], p.x, fma((double)m[5], p.y, fma((double)m[6], p.z, (double)m[7]))),
+                      fma((double)m[8], p.x, fma((double)m[9], p.y, fma((double)m[10], p.z, (double)m[11]))));
+}
 __device__ __forceinline__ float comp(float3 v, int k) { return k == 0 ? v.x : (k == 1 ? v.y : v.z); }
 __device__ __forceinline__ float3 xf_point(const float* m, float3 p) {
   return f3(fmaf(m[0], p.x, fmaf(m[1], p.y, fmaf(m[2], p.z, m[3]))),
@@ -232,8 +248,8 @@ __device__ __forceinline__ float3 camera_dir(const DevScene& S, float sx, float 
   return norm3_exact(S.cf + S.cr * ((2.0f * sx / (float)S.W - 1.0f) * S.tanX) +
                      S.cu * ((1.0f - 2.0f * sy / (float)S.H) * S.tanY));
 }
-__device__ __forceinline__ int project(const DevScene& S, float3 x) {
-  float3 q = x - S.cam_pos;
+__device__ __forceinline__ int project(const DevScene& S, P3 x) {
+  float3 q = sub3(x, p3(S.cam_pos));
   float c = dot3(q, S.cf);
   if (!(c > 0.0f)) return -1;
   float sx = (dot3(q, S.cr) / (c * S.tanX) + 1.0f) * (float)S.W * 0.5f;
@@ -313,57 +329,9 @@ __device__ __forceinline__ void box2(const WRay& r, float4 n0, float4 n1, float4
   t1 = a1;
 }
 
-// Generic BVH2 traversal.  leaf(leaf_index, t) is called for every triangle hit with t in
-// (tmin, tmax); it returns the new tmax (return a negative value to terminate).
 struct TCount {  // traversal work of one thread: internal nodes fetched, triangles tested (64 B / 48 B each)
   uint32_t nodes, tris;
 };
-template <class Leaf>
-__device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay& r, float tmin, float tmax, Leaf leaf,
-                                         TCount& tc) {
-  int stack[RR_STACK];
-  int sp = 0;
-  int node = root;
-  while (true) {
-    if (node >= 0) {
-      tc.nodes++;
-      const float4* nd = S.nodes + 4 * node;
-      float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
-      bool h0, h1;
-      float t0, t1;
-      box2(r, n0, n1, n2, tmin, tmax, h0, h1, t0, t1);
-      int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
-      if (h0 && h1) {
-        if (t1 < t0) {
-          int t = c0;
-          c0 = c1;
-          c1 = t;
-        }
-        if (sp < RR_STACK) stack[sp++] = c1;
-        node = c0;
-        continue;
-      } else if (h0) {
-        node = c0;
-        continue;
-      } else if (h1) {
-        node = c1;
-        continue;
-      }
-    } else {
-      int li = ~node;
-      tc.tris++;
-      const float4* tp = S.ltris + 3 * li;
-      float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
-      float t = tri_hit(r, a, b, c);
-      if (t > tmin && t < tmax) {
-        tmax = leaf(li, t, tmax);
-        if (tmax < 0.0f) return;
-      }
-    }
-    if (sp == 0) return;
-    node = stack[--sp];
-  }
-}
 
 __device__ __forceinline__ int leaf_tri_id(const DevScene& S, int li) { return __float_as_int(__ldg(S.ltris + 3 * li).w); }
 
@@ -394,102 +362,5 @@ struct QCount {  // per-thread query counters
   uint32_t closest, shadow, inst;
   TCount tc;
 };
-
-__device__ __forceinline__ Hit closest_static(const DevScene& S, const WRay& r, float tmin, int excl, TCount& tc) {
-  Hit h;
-  h.t = RR_TMAX;
-  h.leaf = -1;
-  h.inst = -1;
-  if (S.static_root < 0) return h;
-  traverse(S, S.static_root, r, tmin, RR_TMAX, [&](int li, float t, float tmax) {
-    if (leaf_tri_id(S, li) == excl) return tmax;
-    h.t = t;
-    h.leaf = li;
-    return t;
-  }, tc);
-  return h;
-}
-// closest hit among edited instances placed at M_F, beyond tmin and before h.t (updates h)
-__device__ __forceinline__ void closest_dyn(const DevScene& S, int F, float3 o, float3 d, float tmin, int excl, Hit& h,
-                                            TCount& tc) {
-  float3 inv = f3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
-  for (int k = 0; k < S.n_inst; ++k) {
-    const DevInstance& I = S.inst[k];
-    if (!inst_box(I, F, o, inv, tmin, h.t)) continue;
-    WRay r = make_wray(xf_point(I.Mi[F], o), xf_vec(I.Mi[F], d));
-    traverse(S, I.root, r, tmin, h.t, [&](int li, float t, float tmax) {
-      if (leaf_tri_id(S, li) == excl) return tmax;
-      h.t = t;
-      h.leaf = li;
-      h.inst = k;
-      return t;
-    }, tc);
-  }
-}
-
-// ghost crossings in state F: hits of MOVED instances placed at M_Fbar, t in (tmin, tmax); segment
-// length L for the (L - t) sums; hits within dedup_tol of an already counted one count once
-__device__ __forceinline__ Cross crossings(const DevScene& S, int F, float3 o, float3 d, float tmin, float tmax, float L,
-                                           TCount& tc) {
-  Cross c = cross_zero();
-  int Fb = 1 - F;
-  float3 inv = f3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
-  float seen[8];
-  int ns = 0;
-  for (int k = 0; k < S.n_inst; ++k) {
-    const DevInstance& I = S.inst[k];
-    if (!I.moved) continue;
-    if (!inst_box(I, Fb, o, inv, tmin, tmax)) continue;
-    float3 od = xf_vec(I.Mi[Fb], d);
-    WRay r = make_wray(xf_point(I.Mi[Fb], o), od);
-    traverse(S, I.root, r, tmin, tmax, [&](int li, float t, float tm) {
-      for (int q = 0; q < ns; ++q)
-        if (fabsf(seen[q] - t) < S.dedup_tol) return tm;
-      if (ns < 8) seen[ns++] = t;
-      const float4* tp = S.ltris + 3 * li;
-      float4 a = __ldg(tp), b = __ldg(tp + 1), cc = __ldg(tp + 2);
-      float3 nrm = norm3_exact(cross3(f3(b.x - a.x, b.y - a.y, b.z - a.z), f3(cc.x - a.x, cc.y - a.y, cc.z - a.z)));
-      float inv_c = 1.0f / fabsf(dot3(nrm, od));
-      c.n += 1.0f;
-      c.s0 += inv_c;
-      c.sa += t * t * inv_c;
-      c.sb += (L - t) * (L - t) * inv_c;
-      return tm;
-    }, tc);
-  }
-  return c;
-}
-
-// any hit of static geometry in (tmin, tmax) excluding two triangle ids
-__device__ __forceinline__ bool occluded_static(const DevScene& S, const WRay& r, float tmin, float tmax, int ea, int eb,
-                                                TCount& tc) {
-  if (S.static_root < 0) return false;
-  bool hit = false;
-  traverse(S, S.static_root, r, tmin, tmax, [&](int li, float t, float tm) {
-    int id = leaf_tri_id(S, li);
-    if (id == ea || id == eb) return tm;
-    hit = true;
-    return -1.0f;
-  }, tc);
-  return hit;
-}
-__device__ __forceinline__ bool occluded_dyn(const DevScene& S, int F, float3 o, float3 d, float tmin, float tmax, int ea, int eb,
-                                             TCount& tc) {
-  float3 inv = f3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
-  for (int k = 0; k < S.n_inst; ++k) {
-    const DevInstance& I = S.inst[k];
-    if (!inst_box(I, F, o, inv, tmin, tmax)) continue;
-    WRay r = make_wray(xf_point(I.Mi[F], o), xf_vec(I.Mi[F], d));
-    bool hit = false;
-    traverse(S, I.root, r, tmin, tmax, [&](int li, float t, float tm) {
-      int id = leaf_tri_id(S, li);
-      if (id == ea || id == eb) return tm;
-      hit = true;
-      return -1.0f;
-    }, tc);
-    if (hit) return true;
-  }
-  return false;
-}
 
 }  // namespace rr

@@ -16,6 +16,9 @@
 // diverged rough vertex, and connections are evaluated and splatted as soon as they are formed.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "rr_device.cuh"
 #include "rr_kernels.h"
 #include "rr_query.cuh"
@@ -26,7 +29,33 @@ namespace rr {
 #define NQ 10
 #define FULLMASK 0xffffffffu
 
+#ifndef RR_WARP_POOL
+#define RR_WARP_POOL 0  // 1: queries in global slots, traced by the warp's lanes with dynamic fetch
+#endif
+#if RR_WARP_POOL
+// The query batch of one lane lives in global memory (slot k of lane g at k * nlanes + g) so that any
+// lane of the warp can trace it.
+struct QView {
+  Query* p;
+  int stride;
+  __device__ __forceinline__ Query& operator[](int i) const { return p[(size_t)i * stride]; }
+};
+struct RView {
+  const QRes* p;
+  int stride;
+  __device__ __forceinline__ const QRes& operator[](int i) const { return p[(size_t)i * stride]; }
+};
 struct Batch {
+  QView q;
+  RView r;
+  int n;
+  __device__ __forceinline__ int push(const Query& x) {
+    q[n] = x;
+    return n++;
+  }
+};
+#else
+struct Batch {  // the query batch of one lane (thread-local)
   Query q[NQ];
   QRes r[NQ];
   int n;
@@ -35,6 +64,7 @@ struct Batch {
     return n++;
   }
 };
+#endif
 __device__ __forceinline__ int bit(int F) { return 1 << F; }
 
 // ------------------------------------------------------------------------------------------------
@@ -81,7 +111,7 @@ __device__ void start_issue(const DevScene& S, int tech, int F, const float d0[8
       if (S.n_edited == 0) return;
       s.b = sample_set(S, S.edited_tris, S.edited_cdf, S.n_edited, F, d0[0], d0[1], d0[2]);
       s.a = sample_emitter(S, d0[3], d0[4], d0[5], d0[6]);
-      if (!(dot3(s.a.n, s.b.p - s.a.p) > 0.0f)) return;
+      if (!(dot3(s.a.n, sub3(s.b.p, s.a.p)) > 0.0f)) return;
       s.qi = B.push(mk_seg(s.a.p, s.b.p, s.a.tri, s.b.tri, bit(F)));
       return;
     }
@@ -97,7 +127,7 @@ __device__ void start_issue(const DevScene& S, int tech, int F, const float d0[8
       if (S.n_moved == 0) return;
       PV xg = sample_set(S, S.moved_tris, S.moved_cdf, S.n_moved, 1 - F, d0[0], d0[1], d0[2]);
       s.a = sample_emitter(S, d0[3], d0[4], d0[5], d0[6]);
-      float3 dv = xg.p - s.a.p;
+      float3 dv = sub3(xg.p, s.a.p);
       s.dl = sqrtf(dot3(dv, dv));
       if (!(s.dl > S.eps)) return;
       s.dir = dv * (1.0f / s.dl);
@@ -110,7 +140,7 @@ __device__ void start_issue(const DevScene& S, int tech, int F, const float d0[8
       PV xg = sample_set(S, S.moved_tris, S.moved_cdf, S.n_moved, 1 - F, d0[0], d0[1], d0[2]);
       s.pix = project(S, xg.p);
       if (s.pix < 0) return;
-      float3 dv = xg.p - E.p;
+      float3 dv = sub3(xg.p, E.p);
       s.dl = sqrtf(dot3(dv, dv));
       s.dir = dv * (1.0f / s.dl);
       s.qi = B.push(mk_ray(E.p, s.dir, -1, bit(F)));
@@ -133,9 +163,9 @@ __device__ void start_consume(const DevScene& S, int tech, int F, const SStart& 
     W.pixel = tech == 2 ? s.pix : -1;
   } else {
     if (!r.ok[F]) return;
-    float3 o = tech == 4 ? s.a.p : E.p;
+    P3 o = tech == 4 ? s.a.p : E.p;
     PV h = hit_pv(S, r.h[F], o, s.dir, F);
-    float3 q = h.p - o;
+    float3 q = sub3(h.p, o);
     if (!(sqrtf(dot3(q, q)) > s.dl + S.eps)) return;  // the first hit lies beyond x_G
     W.v[0] = tech == 4 ? s.a : E;
     W.v[1] = h;
@@ -207,11 +237,11 @@ __device__ void single_issue(const DevScene& S, const KArgs& A, SState& st, Batc
     Mat mp, mq;
     if (hasP && !st.Pend) {
       mp = load_mat(S, (uint32_t)P.v[m].obj, F);
-      st.okP = bsdf_sample(mp, P.v[m].n, norm3_exact(P.v[m - 1].p - P.v[m].p), d[1], d[2], st.woP);
+      st.okP = bsdf_sample(mp, P.v[m].n, norm3_exact(sub3(P.v[m - 1].p, P.v[m].p)), d[1], d[2], st.woP);
     }
     if (st.qActive) {
       mq = load_mat(S, (uint32_t)Q.v[m].obj, Fb);
-      st.okQ = bsdf_sample(mq, Q.v[m].n, norm3_exact(Q.v[m - 1].p - Q.v[m].p), d[1], d[2], st.woQ);
+      st.okQ = bsdf_sample(mq, Q.v[m].n, norm3_exact(sub3(Q.v[m - 1].p, Q.v[m].p)), d[1], d[2], st.woQ);
     }
     bool dirdiv = st.qActive && hasP && !st.Pend && ((st.okP != st.okQ) || (st.okP && st.okQ && !eq3(st.woP, st.woQ)));
     st.div_m = st.rdiv || vdiff || dirdiv;
@@ -363,7 +393,7 @@ __device__ bool single_consume(const DevScene& S, const KArgs& A, SState& st, co
       const PV& vw = P.v[m];
       const PV& vq = Q.v[m];
       const PV& tg = P.v[m + 1];
-      float3 a = vq.p - tg.p, b = vw.p - tg.p;
+      float3 a = sub3(vq.p, tg.p), b = sub3(vw.p, tg.p);
       float la2 = dot3(a, a), lb2 = dot3(b, b);
       int rs = RJ_NONE;
       if (edited(S, tg.obj)) rs = RJ_TARGET;                                                // (1) P:L406
@@ -428,7 +458,7 @@ __device__ bool single_step(const DevScene& S, const KArgs& A, SState& st, Batch
         int pix = (int)(st.i % (uint64_t)npix);
         st.sp.dir = camera_dir(S, (float)(pix % S.W) + d0[0], (float)(pix / S.W) + d0[1]);
         st.sp.pix = st.sq.pix = pix;
-        st.sp.qi = st.sq.qi = B.push(mk_ray(S.cam_pos, st.sp.dir, -1, 3));
+        st.sp.qi = st.sq.qi = B.push(mk_ray(p3(S.cam_pos), st.sp.dir, -1, 3));
       } else {
         start_issue(S, A.tech, F, d0, st.sp, B);
         start_issue(S, A.tech_q, Fb, d0, st.sq, B);
@@ -589,7 +619,7 @@ __device__ void bidir_issue(const DevScene& S, const KArgs& A, int tech, int F, 
       float d[8];
       rng.dims((uint32_t)((side == 0 ? 0 : 16) + m), d);
       Mat mt = load_mat(S, (uint32_t)W.v[m].obj, F);
-      if (bsdf_sample(mt, W.v[m].n, norm3_exact(W.v[m - 1].p - W.v[m].p), d[1], d[2], W.wd))
+      if (bsdf_sample(mt, W.v[m].n, norm3_exact(sub3(W.v[m - 1].p, W.v[m].p)), d[1], d[2], W.wd))
         W.qw = B.push(mk_ray(W.v[m].p, W.wd, W.v[m].tri, bit(F)));
       else
         W.ended = true;
@@ -767,8 +797,23 @@ __device__ __forceinline__ uint64_t fetch_work(unsigned long long* counter, bool
   return base + __popc(m & ((1u << lane) - 1u));
 }
 
+// ------------------------------------------------------------------------------------------------
+// Warp scheduler.  The 32 lanes of a warp advance their samples in lockstep (the state-machine step code
+// runs converged); the queries the step issued (<= NQ per lane, in global slots) then form the warp's pool,
+// which the warp traces with dynamic fetch: a lane whose query is complete takes the next one of the pool,
+// whoever issued it, so a lane with many queries does not keep the others idle.  Traversal itself is
+// warp-synchronous with leaf postponing (Tracer::run_sync).
+// ------------------------------------------------------------------------------------------------
+#define RR_BLOCK 128
+#ifndef RR_TRACE_SLICE
+#define RR_TRACE_SLICE 16        // traversal steps between job / query transitions
+#endif
+
 template <class State, bool BIDIR>
 __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A) {
+#if RR_WARP_POOL
+  __shared__ uint16_t s_pool[RR_BLOCK / 32][32 * NQ];  // (k << 5) | lane of every query of the warp
+#endif
   Out o;
   o.A = &A;
   o.qc.closest = o.qc.shadow = o.qc.inst = 0;
@@ -777,7 +822,22 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
   for (int r = 0; r < 6; ++r) o.rejby[r] = 0;
   uint32_t nsamp = 0;
   State st;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gw = blockIdx.x * RR_BLOCK + wid * 32;  // global lane id of lane 0 of this warp
   Batch B;
+#if RR_WARP_POOL
+  uint16_t* pool = s_pool[wid];
+  B.q.p = A.qbuf + gw + lane;
+  B.q.stride = A.nlanes;
+  B.r.p = A.rbuf + gw + lane;
+  B.r.stride = A.nlanes;
+#endif
+  B.n = 0;
+#if RR_WARP_POOL
+  Tracer T;
+  T.in_job = false;
+#endif
+  unsigned long long sc[6] = {0, 0, 0, 0, 0, 0};  // scheduler occupancy (rr_stats.sched)
   bool active = false, more = true;
   while (true) {
     // refill: lanes without a sample take the next local slot (warp-aggregated atomics)
@@ -817,12 +877,64 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
         }
       }
     }
+#if RR_WARP_POOL
+    // the warp's query pool
+    int n = active ? B.n : 0, x = n;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      int y = __shfl_up_sync(FULLMASK, x, d);
+      if (lane >= d) x += y;
+    }
+    const int total = __shfl_sync(FULLMASK, x, 31);
+    if (total == 0 && !__any_sync(FULLMASK, active || more)) break;
+    for (int k = 0; k < n; ++k) pool[x - n + k] = (uint16_t)((k << 5) | lane);
+    __syncwarp();
+    if (lane == 0) {
+      sc[0]++;
+      sc[3] += (unsigned)total;
+    }
+    sc[4] += active;
+    // trace the pool: dynamic fetch + warp-synchronous traversal
+    int next = 0, cur = -1, owner = 0;
+    while (true) {
+      const unsigned m = __ballot_sync(FULLMASK, cur < 0);
+      if (m && next < total) {
+        int idx = next + __popc(m & ((1u << lane) - 1u));
+        if (cur < 0 && idx < total) {
+          uint32_t e = pool[idx];
+          owner = (int)(e & 31u);
+          cur = (int)((e >> 5) * (uint32_t)A.nlanes + (uint32_t)(gw + owner));
+          T.begin(S, A.qbuf[cur]);
+        }
+        next += __popc(m);
+      }
+      if (__all_sync(FULLMASK, cur < 0)) break;
+      sc[1] += cur >= 0;
+      sc[5] += lane == 0;
+      if (cur >= 0 && !T.in_job && !T.next_job(S, o.qc)) {
+        QRes r;
+        T.result(r);
+        A.rbuf[cur] = r;
+        cur = -1;
+      }
+      T.run_sync(S, o.qc.tc, RR_TRACE_SLICE);
+    }
+    __syncwarp();
+#else
+    // every lane's queries through the single traversal site, in lockstep over the batch index
     int nmax = (int)__reduce_max_sync(FULLMASK, (unsigned)B.n);
     if (nmax == 0 && !__any_sync(FULLMASK, active || more)) break;
-    // all queries of the warp through the single traversal site
+    const unsigned total = __reduce_add_sync(FULLMASK, (unsigned)B.n);
+    if (lane == 0) {
+      sc[0]++;
+      sc[3] += total;
+    }
+    sc[4] += active;
     for (int k = 0; k < nmax; ++k)
       if (k < B.n) run_query(S, B.q[k], B.r[k], o.qc);
+#endif
     if (active) {
+      sc[2]++;
       bool go;
       if constexpr (BIDIR) go = bidir_step(S, A, st, B, o);
       else go = single_step(S, A, st, B, o);
@@ -847,12 +959,14 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
   warp_add(stt + STAT_OFFSCREEN, o.offscreen);
   warp_add(stt + STAT_ZERO, o.zero);
   for (int r = 0; r < 6; ++r) warp_add(stt + STAT_REJBY + r, o.rejby[r]);
+  for (int r = 0; r < 6; ++r)
+    if (sc[r]) atomicAdd(stt + STAT_SCHED + r, sc[r]);
 }
 
-__global__ void __launch_bounds__(128) k_residual_single(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
+__global__ void __launch_bounds__(RR_BLOCK) k_residual_single(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
   residual_loop<SState, false>(S, A);
 }
-__global__ void __launch_bounds__(128) k_residual_bidir(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
+__global__ void __launch_bounds__(RR_BLOCK) k_residual_bidir(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
   residual_loop<BState, true>(S, A);
 }
 
@@ -864,27 +978,78 @@ __global__ void k_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t 
   out[4 * t] = r.x; out[4 * t + 1] = r.y; out[4 * t + 2] = r.z; out[4 * t + 3] = r.w;
 }
 
-__global__ void k_trace(const __grid_constant__ DevScene S, int F, uint32_t n, const float* rays, float* hits) {
-  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const float* r = rays + 8 * t;
+__device__ __forceinline__ void trace_store(const DevScene& S, int F, const float* r, const QRes& res, float* h) {
   float3 o = f3(r[0], r[1], r[2]);
   float3 d = norm3_exact(f3(r[3], r[4], r[5]));
-  int excl = __float_as_int(r[6]);
-  QCount qc = {};
-  QRes res;
-  run_query(S, mk_ray(o, d, excl, bit(F)), res, qc);
-  float* h = hits + 8 * t;
   if (!res.ok[F]) {
     h[0] = -1.0f;
     return;
   }
-  PV v = hit_pv(S, res.h[F], o, d, F);
-  float3 q = v.p - o;
+  PV v = hit_pv(S, res.h[F], p3(o), d, F);
+  float3 q = sub3(v.p, p3(o));
   h[0] = sqrtf(dot3(q, q));
   h[1] = __int_as_float(v.tri);
-  h[2] = v.p.x; h[3] = v.p.y; h[4] = v.p.z;
+  h[2] = (float)v.p.x; h[3] = (float)v.p.y; h[4] = (float)v.p.z;
   h[5] = v.n.x; h[6] = v.n.y; h[7] = v.n.z;
+}
+__device__ __forceinline__ Query trace_query(const float* r, int F) {
+  float3 o = f3(r[0], r[1], r[2]);
+  float3 d = norm3_exact(f3(r[3], r[4], r[5]));
+  return mk_ray(p3(o), d, __float_as_int(r[6]), bit(F));
+}
+
+__global__ void k_trace(const __grid_constant__ DevScene S, int F, uint32_t n, const float* rays, float* hits) {
+  uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  QCount qc = {};
+  QRes res;
+  run_query(S, trace_query(rays + 8 * t, F), res, qc);
+  trace_store(S, F, rays + 8 * t, res, hits + 8 * t);
+}
+
+// persistent variants: lanes take rays from a global counter as soon as their ray is done (diagnostics)
+__global__ void k_trace_persistent(const __grid_constant__ DevScene S, int F, uint32_t n, const float* rays, float* hits,
+                                   unsigned* counter, int slice) {
+  QCount qc = {};
+  Tracer T;
+  T.in_job = false;
+  int cur = -1;
+  bool more = true;
+  const int lane = threadIdx.x & 31;
+  const bool sync = slice < 0;
+  if (sync) slice = -slice;
+  while (true) {
+    // warp-uniform part: take rays for lanes without one
+    const unsigned m = __ballot_sync(FULLMASK, cur < 0 && more);
+    if (m) {
+      int leader = __ffs(m) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(counter, (unsigned)__popc(m));
+      base = __shfl_sync(FULLMASK, base, leader);
+      if (cur < 0 && more) {
+        unsigned idx = base + __popc(m & ((1u << lane) - 1u));
+        if (idx < n) {
+          cur = (int)idx;
+          T.begin(S, trace_query(rays + 8 * idx, F));
+        } else {
+          more = false;
+        }
+      }
+    }
+    if (__all_sync(FULLMASK, cur < 0)) break;
+    // job / query transitions (divergent, short)
+    if (cur >= 0 && !T.in_job && !T.next_job(S, qc)) {
+      QRes res;
+      T.result(res);
+      trace_store(S, F, rays + 8 * cur, res, hits + 8 * cur);
+      cur = -1;
+    }
+    if (sync) {
+      T.run_sync(S, qc.tc, slice);
+    } else if (cur >= 0 && T.in_job) {
+      T.run(S, qc.tc, slice);
+    }
+  }
 }
 
 __global__ void k_segment(const __grid_constant__ DevScene S, uint32_t n, const float* segs, float* out) {
@@ -893,7 +1058,7 @@ __global__ void k_segment(const __grid_constant__ DevScene S, uint32_t n, const 
   const float* s = segs + 6 * t;
   QCount qc = {};
   QRes r;
-  run_query(S, mk_seg(f3(s[0], s[1], s[2]), f3(s[3], s[4], s[5]), -1, -1, 3), r, qc);
+  run_query(S, mk_seg(p3(f3(s[0], s[1], s[2])), p3(f3(s[3], s[4], s[5])), -1, -1, 3), r, qc);
   float* o = out + 10 * t;
   for (int F = 0; F < 2; ++F) {
     o[5 * F] = r.ok[F] ? 1.0f : 0.0f;
@@ -905,14 +1070,43 @@ __global__ void k_segment(const __grid_constant__ DevScene S, uint32_t n, const 
 }
 
 // ---- host launchers
+size_t query_slot_bytes() { return RR_WARP_POOL ? (size_t)NQ * sizeof(Query) : 0; }
+size_t batch_bytes_per_lane() { return RR_WARP_POOL ? (size_t)NQ * (sizeof(Query) + sizeof(QRes)) : 0; }
+// persistent lanes: one wave of resident blocks on every SM (fewer for tiny launches)
+int residual_grid(bool bidir, uint64_t n) {
+  static int occ[2] = {0, 0}, sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_residual_single, RR_BLOCK, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_residual_bidir, RR_BLOCK, 0);
+  }
+  uint64_t g = (n + RR_BLOCK - 1) / RR_BLOCK;
+  uint64_t cap = (uint64_t)sms * (uint64_t)std::max(1, occ[bidir ? 1 : 0]);
+  return (int)std::max<uint64_t>(1, std::min(g, cap));
+}
+int residual_block() { return RR_BLOCK; }
 void launch_residual(const DevScene& S, const KArgs& A, int grid, cudaStream_t st) {
-  if (A.tech == 3 || A.tech == 6) k_residual_bidir<<<grid, 128, 0, st>>>(S, A);
-  else k_residual_single<<<grid, 128, 0, st>>>(S, A);
+  if (A.tech == 3 || A.tech == 6) k_residual_bidir<<<grid, RR_BLOCK, 0, st>>>(S, A);
+  else k_residual_single<<<grid, RR_BLOCK, 0, st>>>(S, A);
 }
 void launch_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out, cudaStream_t st) {
   k_philox<<<(n + 255) / 256, 256, 0, st>>>(n, ctr, k0, k1, out);
 }
 void launch_trace(const DevScene& S, int F, uint32_t n, const float* rays, float* hits, cudaStream_t st) {
+  const char* mode = getenv("RR_TRACE_MODE");  // diagnostics: persistent dynamic-fetch variant
+  if (mode && atoi(mode) != 0) {
+    static unsigned* counter = nullptr;
+    if (!counter) cudaMalloc(&counter, sizeof(unsigned));
+    cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
+    int sms = 148, occ = 1, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trace_persistent, 128, 0);
+    k_trace_persistent<<<sms * occ, 128, 0, st>>>(S, F, n, rays, hits, counter, atoi(mode));
+    return;
+  }
   k_trace<<<(n + 127) / 128, 128, 0, st>>>(S, F, n, rays, hits);
 }
 void launch_segment(const DevScene& S, uint32_t n, const float* segs, float* out, cudaStream_t st) {

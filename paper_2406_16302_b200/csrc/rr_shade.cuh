@@ -10,7 +10,8 @@ enum { ST_ACCEPTED = 0, ST_REJECTED = 1, ST_UNPAIRED = 2, ST_MAPPED_ONLY = 3 };
 enum { RJ_NONE = 0, RJ_OCCLUDED = 1, RJ_JACOBIAN = 2, RJ_MULTI = 3, RJ_TARGET = 4, RJ_SUFFIX_DYN = 5 };
 
 struct PV {  // path vertex in one state
-  float3 p, n;
+  P3 p;          // position (fp64, see rr_device.cuh)
+  float3 n;
   int tri, obj;  // tri = -1: camera; obj = -1: camera
 };
 
@@ -20,11 +21,11 @@ __device__ __forceinline__ uint32_t oflags(const DevScene& S, int obj);
 // on a moved object lies on a different hit instance in each state)
 __device__ __forceinline__ bool same_pv(const DevScene& S, const PV& a, const PV& b) {
   if (oflags(S, a.obj) & OBJ_MOVED) return false;
-  return a.tri == b.tri && eq3(a.p, b.p) && eq3(a.n, b.n);
+  return a.tri == b.tri && eqp(a.p, b.p) && eq3(a.n, b.n);
 }
 __device__ __forceinline__ PV cam_pv(const DevScene& S) {
   PV v;
-  v.p = S.cam_pos;
+  v.p = p3(S.cam_pos);
   v.n = S.cf;
   v.tri = -1;
   v.obj = -1;
@@ -33,13 +34,26 @@ __device__ __forceinline__ PV cam_pv(const DevScene& S) {
 __device__ __forceinline__ uint32_t oflags(const DevScene& S, int obj) { return obj < 0 ? 0u : __ldg(&S.obj_flags[obj]); }
 __device__ __forceinline__ bool edited(const DevScene& S, int obj) { return (oflags(S, obj) & OBJ_EDITED) != 0u; }
 
-// hit -> vertex in state F
-__device__ __forceinline__ PV hit_pv(const DevScene& S, const Hit& h, float3 o, float3 d, int F) {
+// hit -> vertex in state F: the fp64 intersection of the ray (o, d) with the hit triangle's plane
+__device__ __forceinline__ PV hit_pv(const DevScene& S, const Hit& h, P3 o, float3 d, int F) {
   PV v;
-  v.p = o + d * h.t;
   const float4* tp = S.ltris + 3 * h.leaf;
   float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
   float3 n = cross3(f3(b.x - a.x, b.y - a.y, b.z - a.z), f3(c.x - a.x, c.y - a.y, c.z - a.z));
+  {
+    P3 A = make_double3(a.x, a.y, a.z), B = make_double3(b.x, b.y, b.z), C = make_double3(c.x, c.y, c.z);
+    if (h.inst >= 0) {
+      const float* M = S.inst[h.inst].M[F];
+      A = xf_point_d(M, A);
+      B = xf_point_d(M, B);
+      C = xf_point_d(M, C);
+    }
+    double e1x = B.x - A.x, e1y = B.y - A.y, e1z = B.z - A.z, e2x = C.x - A.x, e2y = C.y - A.y, e2z = C.z - A.z;
+    double nx = e1y * e2z - e1z * e2y, ny = e1z * e2x - e1x * e2z, nz = e1x * e2y - e1y * e2x;
+    double den = nx * d.x + ny * d.y + nz * d.z;
+    double t = (den != 0.0) ? (nx * (A.x - o.x) + ny * (A.y - o.y) + nz * (A.z - o.z)) / den : (double)h.t;
+    v.p = make_double3(o.x + t * d.x, o.y + t * d.y, o.z + t * d.z);
+  }
   if (h.inst >= 0) n = xf_vec(S.inst[h.inst].M[F], n);
   v.n = norm3_exact(n);
   v.tri = __float_as_int(a.w);
@@ -59,12 +73,13 @@ __device__ PV sample_set(const DevScene& S, const uint32_t* tris, const float* c
   float4 a = __ldg(&S.tverts[3 * tri]), b = __ldg(&S.tverts[3 * tri + 1]), c = __ldg(&S.tverts[3 * tri + 2]);
   float su = sqrtf(u1);
   float b0 = 1.0f - su, b1 = u2 * su, b2 = 1.0f - b0 - b1;
-  float3 x = f3(a.x, a.y, a.z) * b0 + f3(b.x, b.y, b.z) * b1 + f3(c.x, c.y, c.z) * b2;
+  P3 x = make_double3((double)a.x * b0 + (double)b.x * b1 + (double)c.x * b2, (double)a.y * b0 + (double)b.y * b1 + (double)c.y * b2,
+                      (double)a.z * b0 + (double)b.z * b1 + (double)c.z * b2);
   float3 nrm = cross3(f3(b.x - a.x, b.y - a.y, b.z - a.z), f3(c.x - a.x, c.y - a.y, c.z - a.z));
   int obj = (int)__ldg(&S.tri_obj[tri]);
   int k = __ldg(&S.obj_inst[obj]);
   if (k >= 0) {
-    x = xf_point(S.inst[k].M[F], x);
+    x = xf_point_d(S.inst[k].M[F], x);
     nrm = xf_vec(S.inst[k].M[F], nrm);
   }
   PV v;
@@ -91,8 +106,8 @@ __device__ __forceinline__ Cross swapc(Cross c) {
 // area pdf of generating `to` from `from` with the walk arriving from `prev` (state F)
 __device__ __forceinline__ float area_pdf(const DevScene& S, int F, const PV& prev, const PV& from, const PV& to) {
   Mat m = load_mat(S, (uint32_t)from.obj, F);
-  float3 wi = norm3_exact(prev.p - from.p);
-  float3 dv = to.p - from.p;
+  float3 wi = norm3_exact(sub3(prev.p, from.p));
+  float3 dv = sub3(to.p, from.p);
   float d2 = dot3(dv, dv);
   float3 wo = dv * (1.0f / sqrtf(d2));
   return bsdf_pdf(m, from.n, wi, wo) * fabsf(dot3(to.n, wo)) / d2;
@@ -105,7 +120,7 @@ __device__ __forceinline__ float area_pdf(const DevScene& S, int F, const PV& pr
 // ------------------------------------------------------------------------------------------------
 __device__ float3 path_value(const DevScene& S, const PV* x, const Cross* e, int k, int F, uint32_t mask) {
   const float3 zero = f3(0.f, 0.f, 0.f);
-  float3 d01 = x[1].p - x[0].p;
+  float3 d01 = sub3(x[1].p, x[0].p);
   float dd01 = dot3(d01, d01);
   float3 w01 = d01 * (1.0f / sqrtf(dd01));
   float cth = dot3(w01, S.cf);
@@ -113,7 +128,7 @@ __device__ float3 path_value(const DevScene& S, const PV* x, const Cross* e, int
   const PV& L = x[k - 1];
   float4 le4 = __ldg(&S.obj_emit[L.obj]);
   float3 Le = f3(le4.x, le4.y, le4.z);
-  if (!(dot3(L.n, x[k - 2].p - L.p) > 0.0f)) return zero;  // front face only
+  if (!(dot3(L.n, sub3(x[k - 2].p, L.p)) > 0.0f)) return zero;  // front face only
   if (k == 2) return Le;                                     // direct view: W_e G / p_cam = 1, Pi = p_T7
   float cos1 = fabsf(dot3(x[1].n, w01));
   float invpcam = S.Aplane * cth * cth * cth * dd01 / cos1;  // 1 / p_cam(x_1)
@@ -125,8 +140,8 @@ __device__ float3 path_value(const DevScene& S, const PV* x, const Cross* e, int
   float Q = 1.0f;  // prod_{m < i} rev_m / fwd_{m+1}
   for (int i = 1; i <= k - 2; ++i) {
     Mat m = load_mat(S, (uint32_t)x[i].obj, F);
-    float3 wi = norm3_exact(x[i - 1].p - x[i].p);
-    float3 dv = x[i + 1].p - x[i].p;
+    float3 wi = norm3_exact(sub3(x[i - 1].p, x[i].p));
+    float3 dv = sub3(x[i + 1].p, x[i].p);
     float d2 = dot3(dv, dv);
     float3 wo = dv * (1.0f / sqrtf(d2));
     float3 rho = bsdf_eval(m, x[i].n, wi, wo);
@@ -152,7 +167,7 @@ __device__ float3 path_value(const DevScene& S, const PV* x, const Cross* e, int
     }
     if (i <= k - 3) {  // q_i = rev_i / fwd_{i+1} on edge (i, i+1)
       Mat mn = load_mat(S, (uint32_t)x[i + 1].obj, F);
-      float pr = bsdf_pdf(mn, x[i + 1].n, norm3_exact(x[i + 2].p - x[i + 1].p), wo * -1.0f);
+      float pr = bsdf_pdf(mn, x[i + 1].n, norm3_exact(sub3(x[i + 2].p, x[i + 1].p)), wo * -1.0f);
       Q *= pr * cout / (pf * cin_next);
     }
   }

@@ -53,11 +53,13 @@ class rr_stats(C.Structure):
                                           "mapped_only", "reconnected", "closest_rays", "shadow_rays",
                                           "instance_queries", "splats", "offscreen", "zero_pairs",
                                           "nodes_visited", "tris_tested")] + \
-               [("rejected_by", C.c_uint64 * 8), ("effective_mask", C.c_uint32), ("n_moved", C.c_uint32)]
+               [("rejected_by", C.c_uint64 * 8), ("effective_mask", C.c_uint32), ("n_moved", C.c_uint32),
+                ("sched", C.c_uint64 * 8)]
 
     def as_dict(self):
-        d = {n: int(getattr(self, n)) for n, _ in self._fields_ if n != "rejected_by"}
+        d = {n: int(getattr(self, n)) for n, _ in self._fields_ if n not in ("rejected_by", "sched")}
         d["rejected_by"] = [int(x) for x in self.rejected_by]
+        d["sched"] = [int(x) for x in self.sched]
         return d
 
 
@@ -79,9 +81,10 @@ def lib() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise RuntimeError(f"CUDA extension missing: {LIB_PATH} (run __graft_entry__.build())")
-    L = C.CDLL(LIB_PATH)
+    path = os.environ.get("RR_LIB_VARIANT") or LIB_PATH  # tuning experiments (tools/variants.py) only
+    if not os.path.exists(path):
+        raise RuntimeError(f"CUDA extension missing: {path} (run __graft_entry__.build())")
+    L = C.CDLL(path)
     P, U32, U64 = C.c_void_p, C.c_uint32, C.c_uint64
     L.rr_create.argtypes = [C.c_int, C.POINTER(P)]
     L.rr_destroy.argtypes = [P]

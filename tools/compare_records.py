@@ -12,7 +12,7 @@ from rr_inputs import scenes as S  # noqa: E402
 
 
 def load(name):
-    return np.load(os.path.join("gpurun_out", f"rec_{name}.npy"))
+    return np.load(os.path.join(os.environ.get("RR_REC_DIR", "gpurun_out"), f"rec_{name}.npy"))
 
 
 def close(g, o, rel=1e-4):
@@ -74,6 +74,8 @@ if __name__ == "__main__":
             w = S.config1(); compare(nm, w, dataclasses.replace(w.args, flags=1), 3000)
         elif nm == "c1d8":
             w = S.config1(32, 32, spp=4, max_depth=8); compare(nm, w, w.args, 1000)
+        elif nm == "c2full":
+            w = S.config2(); compare(nm, w, w.args, 40000, verbose=40)
         elif nm == "c2":
             w = S.config2(); compare(nm, w, w.args, 2000)
         elif nm == "c3":

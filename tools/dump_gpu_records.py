@@ -9,7 +9,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from rr_inputs import scenes as S  # noqa: E402
 from paper_2406_16302_b200 import Renderer  # noqa: E402
 
-OUT = "gpurun_out"
+OUT = os.environ.get("RR_REC_DIR", "gpurun_out")
 
 
 def recs_to_np(recs):
@@ -33,6 +33,10 @@ def dump(name, w, args, n_per):
 
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "c2full":
+        w = S.config2()
+        dump("c2full", w, w.args, 40000)
+        return
     w = S.config1()
     dump("c1_f7", w, w.args, 3000)
     dump("c1_f1", w, dataclasses.replace(w.args, flags=1), 3000)

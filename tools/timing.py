@@ -34,5 +34,9 @@ for k in cfgs:
           f"closest {st['closest_rays']} shadow {st['shadow_rays']} inst {st['instance_queries']} "
           f"Mrays/s {(st['closest_rays'] + st['shadow_rays']) / ms / 1e3:.1f}  nodes {st['nodes_visited']} tris {st['tris_tested']} "
           f"GB/s(alg) {(64 * st['nodes_visited'] + 48 * st['tris_tested']) / ms / 1e6:.1f}", flush=True)
+    sc = st["sched"]
+    if sc[0]:
+        print(f"   sched: queries/round {sc[3] / sc[0]:.1f}, lanes holding {sc[4] / sc[0]:.1f}/32, slices/round "
+              f"{sc[5] / sc[0]:.1f}, lanes tracing per slice {sc[1] / max(1, sc[5]):.1f}/32", flush=True)
     print("   per launch ms:", [round(x, 2) for x in tm[1:15]], " img sum", img[..., :3].sum().item(), flush=True)
     del r
