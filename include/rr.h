@@ -128,9 +128,8 @@ typedef struct {
   uint32_t effective_mask; /* technique mask after auto-disable (T4-T6 off without moved objects) */
   uint32_t n_moved;        /* moved objects in the current edit */
   uint64_t sched[8];       /* warp-scheduler occupancy of the residual kernels (diagnostics): [0] warp
-                              rounds, [1] lanes tracing summed over traversal slices, [2] sample steps,
-                              [3] queries per round summed, [4] lanes holding a sample summed over
-                              rounds, [5] traversal slices */
+                              rounds, [2] sample steps, [3] queries per round summed, [4] lanes holding
+                              a sample summed over rounds ([1], [5..7] reserved, 0) */
 } rr_stats;
 
 /* one record per emitted base connection (C10), for parity tests */

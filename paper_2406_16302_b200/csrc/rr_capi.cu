@@ -39,8 +39,6 @@ struct rr_ctx {
   DevBuf<int> d_obj_inst, obj_emitter, emit_off, emit_cnt;
   DevBuf<float> emit_pL, emit_cdf, edited_cdf, moved_cdf;
   DevBuf<unsigned long long> stats, work;
-  DevBuf<char> batch;   // per-lane query batches of the residual kernels (rr_residual.cu)
-  size_t batch_lanes = 0;
   DevScene S;
   uint32_t last_mask = 0;
   int edited_equals_moved = 0;
@@ -558,20 +556,8 @@ static KArgs make_kargs(rr_ctx* c, const rr_render_args* a, uint32_t mask, int l
   K.stats = c->stats.p;
   return K;
 }
-// grid of one residual launch and its per-lane query batch buffers (grown on demand)
-static int prepare_launch(rr_ctx* c, KArgs& K) {
-  bool bidir = K.tech == 3 || K.tech == 6;
-  int grid = residual_grid(bidir, K.n_local);
-  size_t lanes = std::max((size_t)residual_grid(false, 1ull << 40), (size_t)residual_grid(true, 1ull << 40)) * residual_block();
-  if (c->batch_lanes < lanes) {
-    c->batch.alloc(lanes * batch_bytes_per_lane());
-    c->batch_lanes = lanes;
-  }
-  K.nlanes = grid * residual_block();
-  K.qbuf = reinterpret_cast<Query*>(c->batch.p);
-  K.rbuf = reinterpret_cast<QRes*>(c->batch.p + c->batch_lanes * query_slot_bytes());
-  return grid;
-}
+// grid of one residual launch (persistent lanes, rr_residual.cu)
+static int prepare_launch(rr_ctx*, KArgs& K) { return residual_grid(K.tech == 3 || K.tech == 6, K.n_local); }
 
 rr_status rr_render_residual(rr_ctx* c, const rr_render_args* a, float* d_image, uint64_t stream) {
   if (!c) return RR_E_INVALID;

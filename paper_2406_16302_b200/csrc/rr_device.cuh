@@ -333,7 +333,6 @@ struct TCount {  // traversal work of one thread: internal nodes fetched, triang
   uint32_t nodes, tris;
 };
 
-__device__ __forceinline__ int leaf_tri_id(const DevScene& S, int li) { return __float_as_int(__ldg(S.ltris + 3 * li).w); }
 
 // world AABB of instance k in state F vs ray segment
 __device__ __forceinline__ bool inst_box(const DevInstance& I, int F, float3 o, float3 inv, float tmin, float tmax) {

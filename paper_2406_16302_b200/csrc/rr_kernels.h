@@ -31,16 +31,11 @@ struct KArgs {
   rr_path_record* recs;
   unsigned long long* rec_count;
   uint64_t rec_cap;
-  struct Query* qbuf;                // per-lane query batches: slot k of lane g at k * nlanes + g
-  struct QRes* rbuf;
-  int nlanes;                        // grid * block
 };
 
 void launch_residual(const DevScene& S, const KArgs& A, int grid, cudaStream_t st);
 int residual_grid(bool bidir, uint64_t n);  // blocks of residual_block() threads for n sample slots
 int residual_block();
-size_t batch_bytes_per_lane();               // query + result slots of one lane (global memory)
-size_t query_slot_bytes();                   // query slots of one lane
 void launch_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out, cudaStream_t st);
 void launch_trace(const DevScene& S, int F, uint32_t n, const float* rays, float* hits, cudaStream_t st);
 void launch_segment(const DevScene& S, uint32_t n, const float* segs, float* out, cudaStream_t st);

@@ -17,7 +17,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 
 #include "rr_device.cuh"
 #include "rr_kernels.h"
@@ -29,32 +28,6 @@ namespace rr {
 #define NQ 10
 #define FULLMASK 0xffffffffu
 
-#ifndef RR_WARP_POOL
-#define RR_WARP_POOL 0  // 1: queries in global slots, traced by the warp's lanes with dynamic fetch
-#endif
-#if RR_WARP_POOL
-// The query batch of one lane lives in global memory (slot k of lane g at k * nlanes + g) so that any
-// lane of the warp can trace it.
-struct QView {
-  Query* p;
-  int stride;
-  __device__ __forceinline__ Query& operator[](int i) const { return p[(size_t)i * stride]; }
-};
-struct RView {
-  const QRes* p;
-  int stride;
-  __device__ __forceinline__ const QRes& operator[](int i) const { return p[(size_t)i * stride]; }
-};
-struct Batch {
-  QView q;
-  RView r;
-  int n;
-  __device__ __forceinline__ int push(const Query& x) {
-    q[n] = x;
-    return n++;
-  }
-};
-#else
 struct Batch {  // the query batch of one lane (thread-local)
   Query q[NQ];
   QRes r[NQ];
@@ -64,7 +37,6 @@ struct Batch {  // the query batch of one lane (thread-local)
     return n++;
   }
 };
-#endif
 __device__ __forceinline__ int bit(int F) { return 1 << F; }
 
 // ------------------------------------------------------------------------------------------------
@@ -798,22 +770,18 @@ __device__ __forceinline__ uint64_t fetch_work(unsigned long long* counter, bool
 }
 
 // ------------------------------------------------------------------------------------------------
-// Warp scheduler.  The 32 lanes of a warp advance their samples in lockstep (the state-machine step code
-// runs converged); the queries the step issued (<= NQ per lane, in global slots) then form the warp's pool,
-// which the warp traces with dynamic fetch: a lane whose query is complete takes the next one of the pool,
-// whoever issued it, so a lane with many queries does not keep the others idle.  Traversal itself is
-// warp-synchronous with leaf postponing (Tracer::run_sync).
+// kernel: persistent lanes over this shard's samples of one (technique, side).  The 32 lanes of a warp
+// advance their samples in lockstep, then trace the queries the step issued through the single traversal
+// site (rr_query.cuh).
 // ------------------------------------------------------------------------------------------------
 #define RR_BLOCK 128
-#ifndef RR_TRACE_SLICE
-#define RR_TRACE_SLICE 16        // traversal steps between job / query transitions
+#ifndef RR_MIN_BLOCKS
+#define RR_MIN_BLOCKS 16  // resident blocks per SM requested from the register allocator (32 registers:
+                          // latency hiding beats the spills)
 #endif
 
 template <class State, bool BIDIR>
 __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A) {
-#if RR_WARP_POOL
-  __shared__ uint16_t s_pool[RR_BLOCK / 32][32 * NQ];  // (k << 5) | lane of every query of the warp
-#endif
   Out o;
   o.A = &A;
   o.qc.closest = o.qc.shadow = o.qc.inst = 0;
@@ -822,22 +790,10 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
   for (int r = 0; r < 6; ++r) o.rejby[r] = 0;
   uint32_t nsamp = 0;
   State st;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int gw = blockIdx.x * RR_BLOCK + wid * 32;  // global lane id of lane 0 of this warp
+  const int lane = threadIdx.x & 31;
   Batch B;
-#if RR_WARP_POOL
-  uint16_t* pool = s_pool[wid];
-  B.q.p = A.qbuf + gw + lane;
-  B.q.stride = A.nlanes;
-  B.r.p = A.rbuf + gw + lane;
-  B.r.stride = A.nlanes;
-#endif
   B.n = 0;
-#if RR_WARP_POOL
-  Tracer T;
-  T.in_job = false;
-#endif
-  unsigned long long sc[6] = {0, 0, 0, 0, 0, 0};  // scheduler occupancy (rr_stats.sched)
+  unsigned long long sc[5] = {0, 0, 0, 0, 0};  // scheduler occupancy (rr_stats.sched)
   bool active = false, more = true;
   while (true) {
     // refill: lanes without a sample take the next local slot (warp-aggregated atomics)
@@ -877,50 +833,6 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
         }
       }
     }
-#if RR_WARP_POOL
-    // the warp's query pool
-    int n = active ? B.n : 0, x = n;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      int y = __shfl_up_sync(FULLMASK, x, d);
-      if (lane >= d) x += y;
-    }
-    const int total = __shfl_sync(FULLMASK, x, 31);
-    if (total == 0 && !__any_sync(FULLMASK, active || more)) break;
-    for (int k = 0; k < n; ++k) pool[x - n + k] = (uint16_t)((k << 5) | lane);
-    __syncwarp();
-    if (lane == 0) {
-      sc[0]++;
-      sc[3] += (unsigned)total;
-    }
-    sc[4] += active;
-    // trace the pool: dynamic fetch + warp-synchronous traversal
-    int next = 0, cur = -1, owner = 0;
-    while (true) {
-      const unsigned m = __ballot_sync(FULLMASK, cur < 0);
-      if (m && next < total) {
-        int idx = next + __popc(m & ((1u << lane) - 1u));
-        if (cur < 0 && idx < total) {
-          uint32_t e = pool[idx];
-          owner = (int)(e & 31u);
-          cur = (int)((e >> 5) * (uint32_t)A.nlanes + (uint32_t)(gw + owner));
-          T.begin(S, A.qbuf[cur]);
-        }
-        next += __popc(m);
-      }
-      if (__all_sync(FULLMASK, cur < 0)) break;
-      sc[1] += cur >= 0;
-      sc[5] += lane == 0;
-      if (cur >= 0 && !T.in_job && !T.next_job(S, o.qc)) {
-        QRes r;
-        T.result(r);
-        A.rbuf[cur] = r;
-        cur = -1;
-      }
-      T.run_sync(S, o.qc.tc, RR_TRACE_SLICE);
-    }
-    __syncwarp();
-#else
     // every lane's queries through the single traversal site, in lockstep over the batch index
     int nmax = (int)__reduce_max_sync(FULLMASK, (unsigned)B.n);
     if (nmax == 0 && !__any_sync(FULLMASK, active || more)) break;
@@ -932,7 +844,6 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
     sc[4] += active;
     for (int k = 0; k < nmax; ++k)
       if (k < B.n) run_query(S, B.q[k], B.r[k], o.qc);
-#endif
     if (active) {
       sc[2]++;
       bool go;
@@ -959,14 +870,14 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
   warp_add(stt + STAT_OFFSCREEN, o.offscreen);
   warp_add(stt + STAT_ZERO, o.zero);
   for (int r = 0; r < 6; ++r) warp_add(stt + STAT_REJBY + r, o.rejby[r]);
-  for (int r = 0; r < 6; ++r)
+  for (int r = 0; r < 5; ++r)
     if (sc[r]) atomicAdd(stt + STAT_SCHED + r, sc[r]);
 }
 
-__global__ void __launch_bounds__(RR_BLOCK) k_residual_single(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
+__global__ void __launch_bounds__(RR_BLOCK, RR_MIN_BLOCKS) k_residual_single(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
   residual_loop<SState, false>(S, A);
 }
-__global__ void __launch_bounds__(RR_BLOCK) k_residual_bidir(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
+__global__ void __launch_bounds__(RR_BLOCK, RR_MIN_BLOCKS) k_residual_bidir(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
   residual_loop<BState, true>(S, A);
 }
 
@@ -1007,51 +918,6 @@ __global__ void k_trace(const __grid_constant__ DevScene S, int F, uint32_t n, c
   trace_store(S, F, rays + 8 * t, res, hits + 8 * t);
 }
 
-// persistent variants: lanes take rays from a global counter as soon as their ray is done (diagnostics)
-__global__ void k_trace_persistent(const __grid_constant__ DevScene S, int F, uint32_t n, const float* rays, float* hits,
-                                   unsigned* counter, int slice) {
-  QCount qc = {};
-  Tracer T;
-  T.in_job = false;
-  int cur = -1;
-  bool more = true;
-  const int lane = threadIdx.x & 31;
-  const bool sync = slice < 0;
-  if (sync) slice = -slice;
-  while (true) {
-    // warp-uniform part: take rays for lanes without one
-    const unsigned m = __ballot_sync(FULLMASK, cur < 0 && more);
-    if (m) {
-      int leader = __ffs(m) - 1;
-      unsigned base = 0;
-      if (lane == leader) base = atomicAdd(counter, (unsigned)__popc(m));
-      base = __shfl_sync(FULLMASK, base, leader);
-      if (cur < 0 && more) {
-        unsigned idx = base + __popc(m & ((1u << lane) - 1u));
-        if (idx < n) {
-          cur = (int)idx;
-          T.begin(S, trace_query(rays + 8 * idx, F));
-        } else {
-          more = false;
-        }
-      }
-    }
-    if (__all_sync(FULLMASK, cur < 0)) break;
-    // job / query transitions (divergent, short)
-    if (cur >= 0 && !T.in_job && !T.next_job(S, qc)) {
-      QRes res;
-      T.result(res);
-      trace_store(S, F, rays + 8 * cur, res, hits + 8 * cur);
-      cur = -1;
-    }
-    if (sync) {
-      T.run_sync(S, qc.tc, slice);
-    } else if (cur >= 0 && T.in_job) {
-      T.run(S, qc.tc, slice);
-    }
-  }
-}
-
 __global__ void k_segment(const __grid_constant__ DevScene S, uint32_t n, const float* segs, float* out) {
   uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
@@ -1070,8 +936,6 @@ __global__ void k_segment(const __grid_constant__ DevScene S, uint32_t n, const 
 }
 
 // ---- host launchers
-size_t query_slot_bytes() { return RR_WARP_POOL ? (size_t)NQ * sizeof(Query) : 0; }
-size_t batch_bytes_per_lane() { return RR_WARP_POOL ? (size_t)NQ * (sizeof(Query) + sizeof(QRes)) : 0; }
 // persistent lanes: one wave of resident blocks on every SM (fewer for tiny launches)
 int residual_grid(bool bidir, uint64_t n) {
   static int occ[2] = {0, 0}, sms = 0;
@@ -1095,18 +959,6 @@ void launch_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, ui
   k_philox<<<(n + 255) / 256, 256, 0, st>>>(n, ctr, k0, k1, out);
 }
 void launch_trace(const DevScene& S, int F, uint32_t n, const float* rays, float* hits, cudaStream_t st) {
-  const char* mode = getenv("RR_TRACE_MODE");  // diagnostics: persistent dynamic-fetch variant
-  if (mode && atoi(mode) != 0) {
-    static unsigned* counter = nullptr;
-    if (!counter) cudaMalloc(&counter, sizeof(unsigned));
-    cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
-    int sms = 148, occ = 1, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trace_persistent, 128, 0);
-    k_trace_persistent<<<sms * occ, 128, 0, st>>>(S, F, n, rays, hits, counter, atoi(mode));
-    return;
-  }
   k_trace<<<(n + 127) / 128, 128, 0, st>>>(S, F, n, rays, hits);
 }
 void launch_segment(const DevScene& S, uint32_t n, const float* segs, float* out, cudaStream_t st) {

@@ -19,7 +19,18 @@ cam = w.scene.camera
 o = torch.tensor(cam.pos, dtype=torch.float32, device="cuda")
 look = torch.tensor(cam.look_at, dtype=torch.float32, device="cuda")
 fwd = (look - o) / torch.linalg.norm(look - o)
-d = torch.randn((n, 3), generator=g, device="cuda") * 0.35 + fwd
+coherent = os.environ.get("COHERENT", "0") == "1"
+if coherent:  # pixel-ordered pinhole rays over a square image (adjacent lanes: adjacent pixels)
+    side = int(n ** 0.5)
+    n = side * side
+    up = torch.tensor(cam.up, dtype=torch.float32, device="cuda")
+    right = torch.linalg.cross(fwd, up)
+    right = right / torch.linalg.norm(right)
+    up2 = torch.linalg.cross(right, fwd)
+    ys, xs = torch.meshgrid(torch.linspace(-0.5, 0.5, side, device="cuda"), torch.linspace(-0.5, 0.5, side, device="cuda"), indexing="ij")
+    d = fwd + xs.reshape(-1, 1) * right + ys.reshape(-1, 1) * up2
+else:
+    d = torch.randn((n, 3), generator=g, device="cuda") * 0.35 + fwd
 d = d / torch.linalg.norm(d, dim=1, keepdim=True)
 rays = torch.zeros((n, 8), dtype=torch.float32, device="cuda")
 rays[:, 0:3] = o
@@ -37,4 +48,4 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / reps
 hit = (h[:, 0] >= 0).float().mean().item()
-print(f"config {cfg}: {n} camera rays, {ms:.2f} ms, {n / ms / 1e3:.1f} Mrays/s, hit fraction {hit:.3f}")
+print(f"config {cfg}: {n} {'coherent' if coherent else 'random'} camera rays, {ms:.2f} ms, {n / ms / 1e3:.1f} Mrays/s, hit fraction {hit:.3f}")
