@@ -1,5 +1,5 @@
 // rr_lbvh.cu -- GPU LBVH build (Karras 2012 "Maximizing parallelism in the construction of BVHs,
-// octrees, and k-d trees"): 30-bit Morton codes of triangle centroids, CUB radix sort, binary radix tree
+// octrees, and k-d trees"): 63-bit Morton codes of triangle centroids, CUB radix sort, binary radix tree
 // from longest common prefixes (duplicate keys broken by index), bottom-up AABB refit with atomic
 // arrival counters, and packing into 64-byte BVH2 nodes.  SAH-free by design (north star).
 // Replaces the paper's Embree BVH.
@@ -9,6 +9,17 @@
 #include "rr_internal.h"
 
 namespace rr {
+
+#ifndef RR_MORTON_BITS
+#define RR_MORTON_BITS 63  // 21 bits per axis (30: 10 bits per axis)
+#endif
+#if RR_MORTON_BITS == 63
+typedef unsigned long long MortonKey;
+#define RR_MORTON_CELLS 2097152
+#else
+typedef uint32_t MortonKey;
+#define RR_MORTON_CELLS 1024
+#endif
 
 struct Box {
   float lo[3], hi[3];
@@ -59,8 +70,19 @@ __device__ __forceinline__ uint32_t expand_bits(uint32_t v) {
   return v;
 }
 
+// 21 bits per axis -> 63-bit key
+__device__ __forceinline__ uint64_t expand_bits21(uint64_t v) {
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x1f00000000ffffull;
+  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+
 __global__ void k_morton(const float4* __restrict__ tris, int n, const float* __restrict__ partial, int nblocks,
-                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+                         MortonKey* __restrict__ keys, uint32_t* __restrict__ vals) {
   float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
   for (int b = 0; b < nblocks; ++b)
     for (int a = 0; a < 3; ++a) {
@@ -75,21 +97,29 @@ __global__ void k_morton(const float4* __restrict__ tris, int n, const float* __
   for (int a = 0; a < 3; ++a) {
     float ext = hi[a] - lo[a];
     float u = ext > 0.0f ? (c[a] - lo[a]) / ext : 0.5f;
-    q[a] = (uint32_t)fminf(fmaxf(u * 1024.0f, 0.0f), 1023.0f);
+    q[a] = (uint32_t)fminf(fmaxf(u * (float)RR_MORTON_CELLS, 0.0f), (float)(RR_MORTON_CELLS - 1));
   }
+#if RR_MORTON_BITS == 63
+  keys[k] = (expand_bits21(q[0]) << 2) | (expand_bits21(q[1]) << 1) | expand_bits21(q[2]);
+#else
   keys[k] = (expand_bits(q[0]) << 2) | (expand_bits(q[1]) << 1) | expand_bits(q[2]);
+#endif
   vals[k] = (uint32_t)k;
 }
 
-__device__ __forceinline__ int delta(const uint32_t* keys, int n, int i, int j) {
+__device__ __forceinline__ int delta(const MortonKey* keys, int n, int i, int j) {
   if (j < 0 || j >= n) return -1;
-  uint32_t a = keys[i], b = keys[j];
-  if (a == b) return 32 + __clz((uint32_t)i ^ (uint32_t)j);
+  MortonKey a = keys[i], b = keys[j];
+  if (a == b) return 8 * (int)sizeof(MortonKey) + __clz((uint32_t)i ^ (uint32_t)j);
+#if RR_MORTON_BITS == 63
+  return __clzll((long long)(a ^ b));
+#else
   return __clz(a ^ b);
+#endif
 }
 
 // internal node i of the radix tree: children (encoded: >= 0 internal, < 0 leaf ~k) and parents
-__global__ void k_karras(const uint32_t* __restrict__ keys, int n, int* __restrict__ child, int* __restrict__ parent_int,
+__global__ void k_karras(const MortonKey* __restrict__ keys, int n, int* __restrict__ child, int* __restrict__ parent_int,
                          int* __restrict__ parent_leaf) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n - 1) return;
@@ -193,15 +223,16 @@ int build_lbvh(const float4* d_tris, int n, float4* d_nodes, float4* d_ltris, in
   int nb = (n + TB - 1) / TB;
   int nred = nb < 1024 ? nb : 1024;
   DevBuf<float> partial(6 * nred);
-  DevBuf<uint32_t> keys(n), vals(n), keys2(n), vals2(n);
+  DevBuf<MortonKey> keys(n), keys2(n);
+  DevBuf<uint32_t> vals(n), vals2(n);
   DevBuf<int> child(2 * (n > 1 ? n - 1 : 1)), pint(n > 1 ? n - 1 : 1), pleaf(n), counter(n > 1 ? n - 1 : 1);
   DevBuf<Box> ibox(n > 1 ? n - 1 : 1), lbox(n);
   k_centroid_bounds<<<nred, TB, 0, st>>>(d_tris, n, partial.p);
   k_morton<<<nb, TB, 0, st>>>(d_tris, n, partial.p, nred, keys.p, vals.p);
   size_t tmp_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, keys2.p, vals.p, vals2.p, n, 0, 30, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, keys2.p, vals.p, vals2.p, n, 0, RR_MORTON_BITS, st);
   DevBuf<char> tmp(tmp_bytes);
-  cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, keys2.p, vals.p, vals2.p, n, 0, 30, st);
+  cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys.p, keys2.p, vals.p, vals2.p, n, 0, RR_MORTON_BITS, st);
   cudaMemsetAsync(counter.p, 0, sizeof(int) * (n > 1 ? n - 1 : 1), st);
   cudaMemsetAsync(pint.p, 0xff, sizeof(int) * (n > 1 ? n - 1 : 1), st);
   if (n > 1) k_karras<<<(n - 1 + TB - 1) / TB, TB, 0, st>>>(keys2.p, n, child.p, pint.p, pleaf.p);
