@@ -15,6 +15,7 @@ sample of the same workload; it is the reference arm of the driver's comparison,
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import math
 import os
@@ -261,26 +262,53 @@ def run_ours(a):
     assert abs(samples - total_samples) < 0.5, (samples, total_samples)
     value = total_samples * a.steps / (ms / 1e3)
     mrays = (closest + shadow) * a.steps / (ms / 1e3) / 1e6
-    # ---- roofline of the dominant kernel family (the residual kernels: every launch of the step)
+    # ---- roofline of the dominant kernel: the (technique, both sides) launches with the largest time share.
+    # Its algorithmic bytes = 64 B per BVH2 node fetched + 48 B per triangle tested, counted by
+    # the kernels; attributed to the technique by two extra (untimed) renders, {l, T7} minus {T7}.
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         peaks = json.load(open(peaks_path))
         hbm = float(peaks["hbm_gbs"])
-        peak_src = "measured"
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        hbm, peak_src = 6650.0, "fallback"
-    alg_bytes_step = 64.0 * nodes + 48.0 * tris  # BVH2 node (64 B) and triangle (48 B) fetches, SURVEY 8(d)
-    kms = float(kt.item())
-    achieved = alg_bytes_step / (kms / 1e3) / 1e9 if kms > 0 else None
+        hbm, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    mask = st["effective_mask"]
+    sides = 2 if (args.flags & 1) else 1
+    launch_tech = [l for l in range(1, 8) if (mask >> (l - 1)) & 1 for _ in range(sides)]
+    per_tech_ms = {}
+    for l, x in zip(launch_tech, tm[1:1 + len(launch_tech)]):
+        per_tech_ms[l] = per_tech_ms.get(l, 0.0) + x
+    dom = max(per_tech_ms, key=per_tech_ms.get)
+
+    def counts(m):
+        r.render_residual(dataclasses.replace(args, technique_mask=m), image=img, shard_index=rank, shard_count=world)
+        q = r.get_stats()
+        return q["nodes_visited"], q["tris_tested"]
+
+    n7, t7 = counts(0x40)
+    nd, td = (n7, t7) if dom == 7 else counts(0x40 | (1 << (dom - 1)))
+    if dom != 7:
+        nd, td = nd - n7, td - t7
+    dom_bytes = 64.0 * nd + 48.0 * td                    # per render = both side launches
+    dom_ms = per_tech_ms[dom]
+    dom_launch_ms = dom_ms / sides
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else None
+    kname = "k_residual_bidir" if dom in (3, 6) else "k_residual_single"
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": (achieved / hbm) if achieved else None, "traffic": None,
-                "kernel": "k_residual_single + k_residual_bidir (all launches of one render)",
-                "peak_source": peak_src, "algorithmic_bytes_per_step": alg_bytes_step,
-                "kernel_ms_per_step": kms}
+                "kernel": f"{kname} T{dom} (per launch: one side)", "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": dom_bytes / sides, "launch_ms": dom_launch_ms,
+                "share_of_step": dom_ms / sum(per_tech_ms.values()),
+                "all_launches": {"algorithmic_bytes_per_step": 64.0 * nodes + 48.0 * tris,
+                                 "kernel_ms_per_step": float(kt.item()),
+                                 "achieved_gbs": (64.0 * nodes + 48.0 * tris) / (float(kt.item()) / 1e3) / 1e9}}
     prof = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(prof):
         try:
-            roofline["traffic"] = json.load(open(prof)).get(f"config{a.config}")
+            tr = json.load(open(prof)).get(f"config{a.config}_T{dom}")
+            if tr:
+                roofline["traffic"] = tr["dram_bytes_per_launch"]
+                roofline["traffic_source"] = tr["source"]
         except Exception:
             pass
     # ---- end to end through the public API with host buffers (one render per step)

@@ -484,8 +484,6 @@ struct BSide {  // one sub-walk with its per-vertex connection
   PV v[BMAX + 1];
   Cross ex[BMAX + 1];
   Cross cc[BMAX + 1];  // connection-edge crossings (sensor: from v toward E; NEE: from v toward L)
-  PV L[BMAX + 1];      // NEE vertex (emitter side)
-  int pix[BMAX + 1];   // sensor pixel (sensor side)
   uint8_t vis[BMAX + 1];
   int n, nconn;        // walk vertices; vertices whose connection is done
   bool ended;
@@ -577,13 +575,12 @@ __device__ void bidir_issue(const DevScene& S, const KArgs& A, int tech, int F, 
       int t = W.nconn + 1;
       const PV& v = W.v[t];
       if (side == 0) {
-        W.pix[t] = project(S, v.p);
         W.qc = B.push(mk_seg(v.p, E.p, v.tri, -1, bit(F)));
       } else {
         float d[8];
         rng.dims((uint32_t)(16 + t), d);
-        W.L[t] = sample_emitter(S, d[3], d[4], d[5], d[6]);
-        W.qc = B.push(mk_seg(v.p, W.L[t].p, v.tri, W.L[t].tri, bit(F)));
+        PV Lt = sample_emitter(S, d[3], d[4], d[5], d[6]);  // regenerated from the same slot in bidir_path
+        W.qc = B.push(mk_seg(v.p, Lt.p, v.tri, Lt.tri, bit(F)));
       }
     }
     if (!W.ended && W.n < nmax) {
@@ -628,8 +625,8 @@ __device__ void bidir_consume(const DevScene& S, int F, BPath& G, const Batch& B
   }
 }
 
-// path (E, z_t..z_1, [x_D], y_1..y_s, L) of a two-ended sample
-__device__ int bidir_path(const BPath& G, int tech, int t, int s, const DevScene& S, PV* x, Cross* ce) {
+// path (E, z_t..z_1, [x_D], y_1..y_s, L) of a two-ended sample; L is re-drawn from slot 16 + s
+__device__ int bidir_path(const BPath& G, int tech, int t, int s, const DevScene& S, const Rng& rng, PV* x, Cross* ce) {
   int k = 0;
   x[k] = cam_pv(S);
   ce[k] = swapc(G.A.cc[t]);
@@ -652,7 +649,9 @@ __device__ int bidir_path(const BPath& G, int tech, int t, int s, const DevScene
     ce[k] = (j < s) ? G.B.ex[j + 1] : G.B.cc[s];
     ++k;
   }
-  x[k] = G.B.L[s];
+  float d[8];
+  rng.dims((uint32_t)(16 + s), d);
+  x[k] = sample_emitter(S, d[3], d[4], d[5], d[6]);
   ++k;
   return k;
 }
@@ -677,16 +676,16 @@ __device__ void bidir_finish(const DevScene& S, const KArgs& A, BState& st, Out&
       float3 vp = f3(0.f, 0.f, 0.f), vq = vp;
       int pixp = -1, pixq = -1;
       if (pc) {
-        pixp = P.A.pix[t];
+        pixp = project(S, P.A.v[t].p);
         if (P.A.vis[t] && P.B.vis[s]) {
-          int k = bidir_path(P, l, t, s, S, x, ce);
+          int k = bidir_path(P, l, t, s, S, st.rng, x, ce);
           vp = path_value(S, x, ce, k, F, A.mask);
         }
       }
       if (qc_) {
-        pixq = Q.A.pix[t];
+        pixq = project(S, Q.A.v[t].p);
         if (Q.A.vis[t] && Q.B.vis[s]) {
-          int k = bidir_path(Q, l, t, s, S, x, ce);
+          int k = bidir_path(Q, l, t, s, S, st.rng, x, ce);
           vq = path_value(S, x, ce, k, Fb, A.mask);
         }
       }
