@@ -49,6 +49,10 @@ struct rr_ctx {
   bool ev_init = false;
 };
 
+#ifndef RR_LARGE_FRAC
+#define RR_LARGE_FRAC 0.05  // "large" static triangle: box diagonal > this fraction of the static scene's
+#endif
+
 namespace {
 
 rr_status fail(rr_ctx* c, rr_status s, const std::string& m) {
@@ -272,7 +276,7 @@ rr_status rr_scene_upload(rr_ctx* c, const rr_scene_desc* d) {
       c->edited_cdf.upload(cd.data(), cd.size());
     }
     // ---- BLASes: static (world space) + one per dynamic object (object space)
-    size_t total_nodes = stris.empty() ? 0 : std::max<size_t>(stris.size() - 1, 1);
+    size_t total_nodes = stris.empty() ? 0 : std::max<size_t>(stris.size() - 1, 1) + 2;  // + split root, 2nd BLAS
     size_t total_leaves = stris.size();
     for (auto& v : dtris) {
       total_nodes += std::max<size_t>(v.size() > 0 ? v.size() - 1 : 0, 1);
@@ -293,7 +297,49 @@ rr_status rr_scene_upload(rr_ctx* c, const rr_scene_desc* d) {
       leaf_base += (int)tl.size();
       return root;
     };
-    int static_root = stris.empty() ? -1 : build(stris);
+    // Static BLAS: triangles whose box diagonal exceeds RR_LARGE_FRAC of the static scene's get their own
+    // LBVH under an extra root, so that a few huge triangles (a ground plane, light quads) do not inflate
+    // the boxes of every Morton-ordered subtree they land in (SAH-free).
+    int static_root = -1;
+    if (!stris.empty()) {
+      auto box_of = [&](const std::vector<uint32_t>& tl, float lo[3], float hi[3]) {
+        for (int a = 0; a < 3; ++a) { lo[a] = 3e38f; hi[a] = -3e38f; }
+        for (uint32_t t : tl)
+          for (int v = 0; v < 3; ++v) {
+            const float4& p = tv[3ull * t + v];
+            lo[0] = std::min(lo[0], p.x); hi[0] = std::max(hi[0], p.x);
+            lo[1] = std::min(lo[1], p.y); hi[1] = std::max(hi[1], p.y);
+            lo[2] = std::min(lo[2], p.z); hi[2] = std::max(hi[2], p.z);
+          }
+      };
+      float slo[3], shi[3];
+      box_of(stris, slo, shi);
+      double sd = std::sqrt((double)(shi[0] - slo[0]) * (shi[0] - slo[0]) + (double)(shi[1] - slo[1]) * (shi[1] - slo[1]) +
+                            (double)(shi[2] - slo[2]) * (shi[2] - slo[2]));
+      std::vector<uint32_t> small, large;
+      for (uint32_t t : stris) {
+        float lo[3], hi[3];
+        box_of(std::vector<uint32_t>{t}, lo, hi);
+        double d = std::sqrt((double)(hi[0] - lo[0]) * (hi[0] - lo[0]) + (double)(hi[1] - lo[1]) * (hi[1] - lo[1]) +
+                             (double)(hi[2] - lo[2]) * (hi[2] - lo[2]));
+        (d > RR_LARGE_FRAC * sd ? large : small).push_back(t);
+      }
+      if (large.empty() || small.empty()) {
+        static_root = build(stris);
+      } else {
+        const int top = node_base++;  // the extra root, reserved in total_nodes
+        int rs = build(small), rl = build(large);
+        float a0[3], b0[3], a1[3], b1[3];
+        box_of(small, a0, b0);
+        box_of(large, a1, b1);
+        float4 nd[4] = {make_float4(a0[0], b0[0], a0[1], b0[1]), make_float4(a1[0], b1[0], a1[1], b1[1]),
+                        make_float4(a0[2], b0[2], a1[2], b1[2]), make_float4(0.f, 0.f, 0.f, 0.f)};
+        std::memcpy(&nd[3].x, &rs, 4);
+        std::memcpy(&nd[3].y, &rl, 4);
+        cudaMemcpy(c->nodes.p + 4 * top, nd, sizeof(nd), cudaMemcpyHostToDevice);
+        static_root = top;
+      }
+    }
     c->inst_root.clear();
     c->inst_bbox.clear();
     for (auto& v : dtris) {
