@@ -23,6 +23,7 @@ enum { QT_CLOSEST = 0, QT_SEG = 1 };
 
 
 
+
 struct __align__(16) Query {
   float3 o, d;
   float tmax;            // QT_SEG: segment length L; QT_CLOSEST: unused
@@ -43,8 +44,9 @@ struct __align__(16) QRes {
 // tmax (negative: terminate).  id = the triangle's global id (stored in the first vertex's w).
 // ------------------------------------------------------------------------------------------------
 template <class Leaf>
-__device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay& r, float tmin, float tmax, Leaf leaf,
+__device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay& r_in, float tmin, float tmax, Leaf leaf,
                                          TCount& tc) {
+  const WRay& r = r_in;
   int stack[RR_STACK];
   int sp = 0;
   int node = root;

@@ -132,6 +132,19 @@ class Renderer:
                     "rr_render_residual")
         return image
 
+    def render_sequence(self, frames, args, image=None, shard_index: int = 0, shard_count: int = 1):
+        """Chained residuals of an animation (config 5): frame f applies the edit S_f -> S_f+1
+        (`frames[f]`, a list of edits), renders its residual with seed args.seed + f and adds it to `image`,
+        so that after the last frame image = I_0 + sum_f Delta_f (I_0 = the given image, else 0)."""
+        import dataclasses
+        for f, edits in enumerate(frames):
+            self.set_edit(edits)
+            a = dataclasses.replace(args, seed=int(args.seed) + f)
+            acc = image is not None
+            image = self.render_residual(a, image=image, shard_index=shard_index, shard_count=shard_count,
+                                         accumulate=acc)
+        return image
+
     def render_residual_host(self, args, out: Optional[np.ndarray] = None, shard_index: int = 0,
                              shard_count: int = 1) -> np.ndarray:
         """Render into HOST memory (the library copies the image back; blocking)."""

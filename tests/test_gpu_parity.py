@@ -198,12 +198,36 @@ def test_records_occluder_reveal(torch_cuda):
     record_parity(w, w.args)
 
 
-@pytest.mark.parametrize("cfg", [3, 4])
+@pytest.mark.parametrize("cfg", [3, 4, 5])
 def test_records_full_size_configs_sampled(torch_cuda, cfg):
     """Full BASELINE sizes (scene, camera, resolution, D) -- the first indices of every (technique,
-    side), computed one by one by the oracle."""
+    side), computed one by one by the oracle.  Config 5: frame 0 of the animation (3 moved objects)."""
     w = S.load_config(cfg)
-    record_parity(w, w.args, n_per=3000)
+    record_parity(w, w.args, n_per=3000 if cfg != 5 else 2000)
+
+
+def test_records_config5_late_frame(torch_cuda):
+    """Config 5, frame 11 (edits S_11 -> S_12, seed 5000 + 11): every object has moved by 11 steps."""
+    w = S.config5()
+    f = 11
+    w = dataclasses.replace(w, edits=w.frames[f], args=dataclasses.replace(w.args, seed=w.args.seed + f))
+    record_parity(w, w.args, n_per=1000)
+
+
+def test_config5_chain_is_sum_of_frames(torch_cuda):
+    """render_sequence(frames) = sum of the per-frame residuals (accumulation on the device; fp32 adds)."""
+    torch = torch_cuda
+    w = S.config5(64, 36, spp=4, max_depth=4, n_frames=4)
+    r = _renderer(w)
+    chain = r.render_sequence(w.frames, w.args).clone()
+    acc = torch.zeros_like(chain)
+    for f, ed in enumerate(w.frames):
+        r.set_edit(ed)
+        acc += r.render_residual(dataclasses.replace(w.args, seed=w.args.seed + f))
+    torch.cuda.synchronize()
+    scale = float(acc.abs().max())
+    assert scale > 0
+    assert float((chain - acc).abs().max()) <= 1e-5 * scale
 
 
 # ---------------------------------------------------------------- images and exact special cases
