@@ -280,11 +280,13 @@ def run_ours(a):
         per_tech_ms[l] = per_tech_ms.get(l, 0.0) + x
     dom = max(per_tech_ms, key=per_tech_ms.get)
 
-    def counts(m):
-        r.render_residual(dataclasses.replace(args, technique_mask=m), image=img, shard_index=rank, shard_count=world)
+    def counts(m):  # untimed render with traversal counting
+        r.render_residual(dataclasses.replace(args, technique_mask=m), image=img, shard_index=rank, shard_count=world,
+                          count_traversal=True)
         q = r.get_stats()
         return q["nodes_visited"], q["tris_tested"]
 
+    nodes, tris = counts(args.technique_mask)  # all launches of the step
     n7, t7 = counts(0x40)
     nd, td = (n7, t7) if dom == 7 else counts(0x40 | (1 << (dom - 1)))
     if dom != 7:

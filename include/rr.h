@@ -96,7 +96,8 @@ enum {
   RR_TWO_WAY = 1u,     /* sample both states, half the budget each (C8) */
   RR_RECONNECT = 2u,   /* "keep vertex the same" reconnection; requires RR_TWO_WAY */
   RR_REJECT_MULTI = 4u,/* reject diverged pairs with >= 2 dynamic vertices; requires RR_TWO_WAY */
-  RR_ACCUMULATE = 8u   /* add into d_image instead of overwriting it */
+  RR_ACCUMULATE = 8u,  /* add into d_image instead of overwriting it */
+  RR_COUNT_TRAVERSAL = 16u /* count BVH node fetches / triangle tests into rr_stats (diagnostic, ~3% slower) */
 };
 #define RR_PAPER_FLAGS (RR_TWO_WAY | RR_RECONNECT | RR_REJECT_MULTI)
 #define RR_MAX_DEPTH 10
@@ -122,8 +123,8 @@ typedef struct {
   uint64_t shadow_rays;    /* any-hit (connection) queries traversing the static BLAS */
   uint64_t instance_queries; /* dynamic-instance-only queries (crossings / re-checks), not in Mrays */
   uint64_t splats, offscreen, zero_pairs;
-  uint64_t nodes_visited;  /* BVH2 internal nodes fetched (64 B each), all traversals */
-  uint64_t tris_tested;    /* leaf triangles tested (48 B each), all traversals */
+  uint64_t nodes_visited;  /* BVH2 internal nodes fetched (64 B each), all traversals (RR_COUNT_TRAVERSAL, else 0) */
+  uint64_t tris_tested;    /* leaf triangles tested (48 B each), all traversals (RR_COUNT_TRAVERSAL, else 0) */
   uint64_t rejected_by[8]; /* by reason: 1 occluded, 2 jacobian, 3 multi, 4 target, 5 suffix-dynamic */
   uint32_t effective_mask; /* technique mask after auto-disable (T4-T6 off without moved objects) */
   uint32_t n_moved;        /* moved objects in the current edit */

@@ -584,6 +584,7 @@ static KArgs make_kargs(rr_ctx* c, const rr_render_args* a, uint32_t mask, int l
   K.max_depth = (int)a->max_depth;
   K.mask = mask;
   K.two_way = (a->flags & RR_TWO_WAY) ? 1 : 0;
+  K.count = (a->flags & RR_COUNT_TRAVERSAL) ? 1 : 0;
   K.reconnect = (a->flags & RR_RECONNECT) ? 1 : 0;
   K.reject_multi = (a->flags & RR_REJECT_MULTI) ? 1 : 0;
   K.seed = a->seed;

@@ -27,6 +27,7 @@ struct KArgs {
   unsigned long long* stats;         // STAT_COUNT counters
   unsigned long long* work;          // sample-slot counter of this launch (zeroed before the launch)
   int dump;
+  int count;                         // count node fetches / triangle tests (RR_COUNT_TRAVERSAL)
   uint64_t i_begin;
   rr_path_record* recs;
   unsigned long long* rec_count;

@@ -24,6 +24,7 @@ enum { QT_CLOSEST = 0, QT_SEG = 1 };
 
 
 
+
 struct __align__(16) Query {
   float3 o, d;
   float tmax;            // QT_SEG: segment length L; QT_CLOSEST: unused
@@ -43,7 +44,7 @@ struct __align__(16) QRes {
 // pushed.  leaf(li, t, tmax, id) is called for every triangle hit with t in (tmin, tmax) and returns the new
 // tmax (negative: terminate).  id = the triangle's global id (stored in the first vertex's w).
 // ------------------------------------------------------------------------------------------------
-template <class Leaf>
+template <bool COUNT, class Leaf>
 __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay& r_in, float tmin, float tmax, Leaf leaf,
                                          TCount& tc) {
   const WRay& r = r_in;
@@ -53,7 +54,7 @@ __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay
   uint32_t nn = 0, nt = 0;
   while (true) {
     if (node >= 0) {
-      nn++;
+      if (COUNT) nn++;
       const float4* nd = S.nodes + 4 * node;
       float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
       bool h0, h1;
@@ -78,7 +79,7 @@ __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay
       }
     } else {
       int li = ~node;
-      nt++;
+      if (COUNT) nt++;
       const float4* tp = S.ltris + 3 * li;
       float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
       float t = tri_hit(r, a, b, c);
@@ -94,7 +95,11 @@ __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay
   tc.tris += nt;
 }
 
-__device__ __noinline__ void run_query(const DevScene& S, const Query& q, QRes& r, QCount& qc) {
+// COUNT: count node fetches and triangle tests (rr_stats.nodes_visited / tris_tested; off in timed renders,
+// where the two counters cost ~3%).  Inlined into its call site: under the 32-register budget a call boundary
+// forces the scene pointers through generic loads and spills (-9% on config 4 when inlined).
+template <bool COUNT>
+__device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRes& r, QCount& qc) {
   const bool seg = q.type == QT_SEG;
   const float L = q.tmax;
   r.ok[0] = r.ok[1] = 0;
@@ -153,7 +158,7 @@ __device__ __noinline__ void run_query(const DevScene& S, const Query& q, QRes& 
     }
     const float Lc = seg ? L : best_t[F];  // segment length for the (L - t) crossing sums
     WRay wr = make_wray(o, d);
-    traverse(S, root, wr, tmin, tmax, [&](int li, float t, float tm, int id) -> float {
+    traverse<COUNT>(S, root, wr, tmin, tmax, [&](int li, float t, float tm, int id) -> float {
       if (kind == 2) {  // ghost crossing (all hits, dedup within dedup_tol)
         for (int a = 0; a < ns; ++a)
           if (fabsf(seen[a] - t) < S.dedup_tol) return tm;

@@ -779,7 +779,7 @@ __device__ __forceinline__ uint64_t fetch_work(unsigned long long* counter, bool
                           // latency hiding beats the spills)
 #endif
 
-template <class State, bool BIDIR>
+template <class State, bool BIDIR, bool COUNT>
 __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A) {
   Out o;
   o.A = &A;
@@ -842,7 +842,7 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
     }
     sc[4] += active;
     for (int k = 0; k < nmax; ++k)
-      if (k < B.n) run_query(S, B.q[k], B.r[k], o.qc);
+      if (k < B.n) run_query<COUNT>(S, B.q[k], B.r[k], o.qc);
     if (active) {
       sc[2]++;
       bool go;
@@ -873,11 +873,13 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
     if (sc[r]) atomicAdd(stt + STAT_SCHED + r, sc[r]);
 }
 
+template <bool COUNT>
 __global__ void __launch_bounds__(RR_BLOCK, RR_MIN_BLOCKS) k_residual_single(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
-  residual_loop<SState, false>(S, A);
+  residual_loop<SState, false, COUNT>(S, A);
 }
+template <bool COUNT>
 __global__ void __launch_bounds__(RR_BLOCK, RR_MIN_BLOCKS) k_residual_bidir(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
-  residual_loop<BState, true>(S, A);
+  residual_loop<BState, true, COUNT>(S, A);
 }
 
 __global__ void k_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out) {
@@ -913,7 +915,7 @@ __global__ void k_trace(const __grid_constant__ DevScene S, int F, uint32_t n, c
   if (t >= n) return;
   QCount qc = {};
   QRes res;
-  run_query(S, trace_query(rays + 8 * t, F), res, qc);
+  run_query<true>(S, trace_query(rays + 8 * t, F), res, qc);
   trace_store(S, F, rays + 8 * t, res, hits + 8 * t);
 }
 
@@ -923,7 +925,7 @@ __global__ void k_segment(const __grid_constant__ DevScene S, uint32_t n, const 
   const float* s = segs + 6 * t;
   QCount qc = {};
   QRes r;
-  run_query(S, mk_seg(p3(f3(s[0], s[1], s[2])), p3(f3(s[3], s[4], s[5])), -1, -1, 3), r, qc);
+  run_query<true>(S, mk_seg(p3(f3(s[0], s[1], s[2])), p3(f3(s[3], s[4], s[5])), -1, -1, 3), r, qc);
   float* o = out + 10 * t;
   for (int F = 0; F < 2; ++F) {
     o[5 * F] = r.ok[F] ? 1.0f : 0.0f;
@@ -942,8 +944,8 @@ int residual_grid(bool bidir, uint64_t n) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_residual_single, RR_BLOCK, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_residual_bidir, RR_BLOCK, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_residual_single<false>, RR_BLOCK, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_residual_bidir<false>, RR_BLOCK, 0);
   }
   uint64_t g = (n + RR_BLOCK - 1) / RR_BLOCK;
   uint64_t cap = (uint64_t)sms * (uint64_t)std::max(1, occ[bidir ? 1 : 0]);
@@ -951,8 +953,14 @@ int residual_grid(bool bidir, uint64_t n) {
 }
 int residual_block() { return RR_BLOCK; }
 void launch_residual(const DevScene& S, const KArgs& A, int grid, cudaStream_t st) {
-  if (A.tech == 3 || A.tech == 6) k_residual_bidir<<<grid, RR_BLOCK, 0, st>>>(S, A);
-  else k_residual_single<<<grid, RR_BLOCK, 0, st>>>(S, A);
+  const bool bidir = A.tech == 3 || A.tech == 6;
+  if (A.count) {
+    if (bidir) k_residual_bidir<true><<<grid, RR_BLOCK, 0, st>>>(S, A);
+    else k_residual_single<true><<<grid, RR_BLOCK, 0, st>>>(S, A);
+  } else {
+    if (bidir) k_residual_bidir<false><<<grid, RR_BLOCK, 0, st>>>(S, A);
+    else k_residual_single<false><<<grid, RR_BLOCK, 0, st>>>(S, A);
+  }
 }
 void launch_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out, cudaStream_t st) {
   k_philox<<<(n + 255) / 256, 256, 0, st>>>(n, ctr, k0, k1, out);

@@ -116,8 +116,9 @@ class Renderer:
         return r
 
     def render_residual(self, args, image=None, stream: Optional[int] = None, shard_index: int = 0,
-                        shard_count: int = 1, accumulate: bool = False):
-        """Render into a torch float32 (H, W, 4) CUDA tensor (allocated if None); asynchronous."""
+                        shard_count: int = 1, accumulate: bool = False, count_traversal: bool = False):
+        """Render into a torch float32 (H, W, 4) CUDA tensor (allocated if None); asynchronous.
+        count_traversal: also count BVH node fetches / triangle tests into get_stats() (diagnostic)."""
         import torch
         if image is None:
             image = torch.empty((self.height, self.width, 4), dtype=torch.float32, device=f"cuda:{self.device}")
@@ -126,6 +127,8 @@ class Renderer:
         a = self.make_args(args, shard_index, shard_count)
         if accumulate:
             a.flags |= N.RR_ACCUMULATE
+        if count_traversal:
+            a.flags |= N.RR_COUNT_TRAVERSAL
         if stream is None:
             stream = torch.cuda.current_stream(self.device).cuda_stream
         self._check(self._L.rr_render_residual(self.h, C.byref(a), image.data_ptr(), int(stream)),

@@ -27,8 +27,9 @@ for k in cfgs:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    st = r.get_stats()
     tm = r.last_timings(16)
+    r.render_residual(w.args, image=img, count_traversal=True)  # node / triangle counts (untimed)
+    st = r.get_stats()
     n = st["samples"]
     print(f"config {k}: upload+lbvh {t_up:.2f}s  render {ms:.1f} ms  samples {n} ({n / ms / 1e3:.1f} M/s)  "
           f"closest {st['closest_rays']} shadow {st['shadow_rays']} inst {st['instance_queries']} "
