@@ -34,7 +34,7 @@ struct rr_ctx {
   std::vector<int> inst_root;
   std::vector<float> inst_bbox;   // 6 per instance, object space
   // device buffers
-  DevBuf<float4> nodes, ltris, tverts, mat, obj_emit;
+  DevBuf<float4> nodes, ltris, lxf, tverts, mat, obj_emit;
   DevBuf<uint32_t> d_tri_obj, obj_flags, mat_type, obj_mat0, obj_mat1, emit_tris, edited_tris, moved_tris;
   DevBuf<int> d_obj_inst, obj_emitter, emit_off, emit_cnt;
   DevBuf<float> emit_pL, emit_cdf, edited_cdf, moved_cdf;
@@ -284,6 +284,7 @@ rr_status rr_scene_upload(rr_ctx* c, const rr_scene_desc* d) {
     }
     c->nodes.alloc(4 * total_nodes);
     c->ltris.alloc(3 * total_leaves);
+    c->lxf.alloc(3 * total_leaves);
     cudaStream_t st = 0;
     int node_base = 0, leaf_base = 0;
     auto build = [&](const std::vector<uint32_t>& tl) {
@@ -292,7 +293,7 @@ rr_status rr_scene_upload(rr_ctx* c, const rr_scene_desc* d) {
         for (int v = 0; v < 3; ++v) tb[3 * k + v] = tv[3ull * tl[k] + v];
       DevBuf<float4> dt;
       dt.upload(tb.data(), tb.size());
-      int root = build_lbvh(dt.p, (int)tl.size(), c->nodes.p, c->ltris.p, node_base, leaf_base, st);
+      int root = build_lbvh(dt.p, (int)tl.size(), c->nodes.p, c->ltris.p, c->lxf.p, node_base, leaf_base, st);
       node_base += (int)std::max<size_t>(tl.size() - 1, 1);
       leaf_base += (int)tl.size();
       return root;
@@ -363,6 +364,7 @@ rr_status rr_scene_upload(rr_ctx* c, const rr_scene_desc* d) {
     std::memset(&S, 0, sizeof(S));
     S.nodes = c->nodes.p;
     S.ltris = c->ltris.p;
+    S.lxf = c->lxf.p;
     S.static_root = static_root;
     S.n_inst = (int)c->dyn_objects.size();
     S.tverts = c->tverts.p;

@@ -52,7 +52,6 @@ __device__ __forceinline__ P3 xf_point_d(const float* m, P3 p) {
                       fma((double)m[4], p.x, fma((double)m[5], p.y, fma((double)m[6], p.z, (double)m[7]))),
                       fma((double)m[8], p.x, fma((double)m[9], p.y, fma((double)m[10], p.z, (double)m[11]))));
 }
-__device__ __forceinline__ float comp(float3 v, int k) { return k == 0 ? v.x : (k == 1 ? v.y : v.z); }
 __device__ __forceinline__ float3 xf_point(const float* m, float3 p) {
   return f3(fmaf(m[0], p.x, fmaf(m[1], p.y, fmaf(m[2], p.z, m[3]))),
             fmaf(m[4], p.x, fmaf(m[5], p.y, fmaf(m[6], p.z, m[7]))),
@@ -122,6 +121,7 @@ struct DevInstance {
 struct DevScene {
   const float4* nodes;
   const float4* ltris;
+  const float4* lxf;          // [3 per leaf] world->unit-triangle rows (rr_lbvh.cu unit_triangle)
   int static_root;  // -1: no static geometry
   int n_inst;
   DevInstance inst[RR_MAX_INST];
@@ -260,55 +260,17 @@ __device__ __forceinline__ int project(const DevScene& S, P3 x) {
 }
 
 // ------------------------------------------------------------------------------------------------
-// ray / triangle (watertight, Woop-Benthin-Wald 2013) and ray / box
+// ray / box.  The ray / triangle test is the unit-triangle test of rr_query.cuh (rows built by rr_lbvh.cu).
 // ------------------------------------------------------------------------------------------------
 struct WRay {
   float3 o, d, inv;
-  int kx, ky, kz;
-  float Sx, Sy, Sz;
 };
 __device__ __forceinline__ WRay make_wray(float3 o, float3 d) {
   WRay r;
   r.o = o;
   r.d = d;
   r.inv = f3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
-  float ax = fabsf(d.x), ay = fabsf(d.y), az = fabsf(d.z);
-  int kz = (ax > ay) ? (ax > az ? 0 : 2) : (ay > az ? 1 : 2);
-  int kx = kz == 2 ? 0 : kz + 1;
-  int ky = kx == 2 ? 0 : kx + 1;
-  if (comp(d, kz) < 0.0f) {
-    int t = kx;
-    kx = ky;
-    ky = t;
-  }
-  r.kx = kx; r.ky = ky; r.kz = kz;
-  float dz = comp(d, kz);
-  r.Sx = comp(d, kx) / dz;
-  r.Sy = comp(d, ky) / dz;
-  r.Sz = 1.0f / dz;
   return r;
-}
-// returns t (> 0) or -1
-__device__ __forceinline__ float tri_hit(const WRay& r, float4 a4, float4 b4, float4 c4) {
-  float3 A = f3(a4.x, a4.y, a4.z) - r.o, B = f3(b4.x, b4.y, b4.z) - r.o, C = f3(c4.x, c4.y, c4.z) - r.o;
-  float Az = comp(A, r.kz), Bz = comp(B, r.kz), Cz = comp(C, r.kz);
-  float Ax = comp(A, r.kx) - r.Sx * Az, Ay = comp(A, r.ky) - r.Sy * Az;
-  float Bx = comp(B, r.kx) - r.Sx * Bz, By = comp(B, r.ky) - r.Sy * Bz;
-  float Cx = comp(C, r.kx) - r.Sx * Cz, Cy = comp(C, r.ky) - r.Sy * Cz;
-  float U = Cx * By - Cy * Bx, V = Ax * Cy - Ay * Cx, W = Bx * Ay - By * Ax;
-  if (U == 0.0f || V == 0.0f || W == 0.0f) {  // fall back to double on edges (watertightness)
-    double CxBy = (double)Cx * By, CyBx = (double)Cy * Bx;
-    U = (float)(CxBy - CyBx);
-    double AxCy = (double)Ax * Cy, AyCx = (double)Ay * Cx;
-    V = (float)(AxCy - AyCx);
-    double BxAy = (double)Bx * Ay, ByAx = (double)By * Ax;
-    W = (float)(BxAy - ByAx);
-  }
-  if ((U < 0.0f || V < 0.0f || W < 0.0f) && (U > 0.0f || V > 0.0f || W > 0.0f)) return -1.0f;
-  float det = U + V + W;
-  if (det == 0.0f) return -1.0f;
-  float T = U * (r.Sz * Az) + V * (r.Sz * Bz) + W * (r.Sz * Cz);
-  return T / det;
 }
 __device__ __forceinline__ void box2(const WRay& r, float4 n0, float4 n1, float4 n2, float tmin, float tmax,
                                      bool& h0, bool& h1, float& t0, float& t1) {

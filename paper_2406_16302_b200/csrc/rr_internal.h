@@ -44,7 +44,7 @@ struct DevBuf {
   }
 };
 
-int build_lbvh(const float4* d_tris, int n, float4* d_nodes, float4* d_ltris, int node_base, int leaf_base,
-               cudaStream_t st);
+int build_lbvh(const float4* d_tris, int n, float4* d_nodes, float4* d_ltris, float4* d_lxf, int node_base,
+               int leaf_base, cudaStream_t st);
 
 }  // namespace rr

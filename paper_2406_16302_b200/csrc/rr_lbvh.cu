@@ -181,15 +181,38 @@ __global__ void k_refit(const float4* __restrict__ tris, const uint32_t* __restr
   }
 }
 
+// world -> unit-triangle affine map of a triangle (Woop 2004): rows r_k with translation, computed in fp64;
+// a point x on the triangle's plane has barycentrics (r0 . x + w0, r1 . x + w1), and r2 . x + w2 is its
+// signed distance to the plane in units of |e1 x e2|^-1.  Degenerate triangles get NaN rows (never hit).
+__device__ void unit_triangle(float4 a, float4 b, float4 c, float4* out) {
+  double ax = a.x, ay = a.y, az = a.z;
+  double e1x = b.x - ax, e1y = b.y - ay, e1z = b.z - az, e2x = c.x - ax, e2y = c.y - ay, e2z = c.z - az;
+  double nx = e1y * e2z - e1z * e2y, ny = e1z * e2x - e1x * e2z, nz = e1x * e2y - e1y * e2x;
+  double det = nx * nx + ny * ny + nz * nz;
+  if (!(det > 0.0)) {
+    for (int r = 0; r < 3; ++r) out[r] = make_float4(0.0f, 0.0f, 0.0f, __int_as_float(0x7fc00000));
+    return;
+  }
+  double inv = 1.0 / det;
+  double r0x = (e2y * nz - e2z * ny) * inv, r0y = (e2z * nx - e2x * nz) * inv, r0z = (e2x * ny - e2y * nx) * inv;
+  double r1x = (ny * e1z - nz * e1y) * inv, r1y = (nz * e1x - nx * e1z) * inv, r1z = (nx * e1y - ny * e1x) * inv;
+  double r2x = nx * inv, r2y = ny * inv, r2z = nz * inv;
+  out[0] = make_float4((float)r0x, (float)r0y, (float)r0z, (float)(-(r0x * ax + r0y * ay + r0z * az)));
+  out[1] = make_float4((float)r1x, (float)r1y, (float)r1z, (float)(-(r1x * ax + r1y * ay + r1z * az)));
+  out[2] = make_float4((float)r2x, (float)r2y, (float)r2z, (float)(-(r2x * ax + r2y * ay + r2z * az)));
+}
+
 __global__ void k_pack(const float4* __restrict__ tris, const uint32_t* __restrict__ order, int n,
                        const int* __restrict__ child, const Box* __restrict__ ibox, const Box* __restrict__ lbox,
-                       float4* __restrict__ nodes, float4* __restrict__ ltris, int node_base, int leaf_base) {
+                       float4* __restrict__ nodes, float4* __restrict__ ltris, float4* __restrict__ lxf, int node_base,
+                       int leaf_base) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) {
     uint32_t t = order[k];
     ltris[3 * (leaf_base + k)] = tris[3 * t];
     ltris[3 * (leaf_base + k) + 1] = tris[3 * t + 1];
     ltris[3 * (leaf_base + k) + 2] = tris[3 * t + 2];
+    unit_triangle(tris[3 * t], tris[3 * t + 1], tris[3 * t + 2], lxf + 3 * (leaf_base + k));
   }
   int ninternal = n > 1 ? n - 1 : 1;
   if (k >= ninternal) return;
@@ -217,8 +240,8 @@ __global__ void k_pack(const float4* __restrict__ tris, const uint32_t* __restri
 
 // Build one BLAS over n >= 1 triangles (3 float4 each, device).  Writes max(n-1,1) nodes at node_base and n
 // leaf triangles at leaf_base.  Returns the root node index (node_base).
-int build_lbvh(const float4* d_tris, int n, float4* d_nodes, float4* d_ltris, int node_base, int leaf_base,
-               cudaStream_t st) {
+int build_lbvh(const float4* d_tris, int n, float4* d_nodes, float4* d_ltris, float4* d_lxf, int node_base,
+               int leaf_base, cudaStream_t st) {
   const int TB = 256;
   int nb = (n + TB - 1) / TB;
   int nred = nb < 1024 ? nb : 1024;
@@ -237,7 +260,7 @@ int build_lbvh(const float4* d_tris, int n, float4* d_nodes, float4* d_ltris, in
   cudaMemsetAsync(pint.p, 0xff, sizeof(int) * (n > 1 ? n - 1 : 1), st);
   if (n > 1) k_karras<<<(n - 1 + TB - 1) / TB, TB, 0, st>>>(keys2.p, n, child.p, pint.p, pleaf.p);
   k_refit<<<nb, TB, 0, st>>>(d_tris, vals2.p, n, child.p, pint.p, pleaf.p, ibox.p, lbox.p, counter.p);
-  k_pack<<<nb, TB, 0, st>>>(d_tris, vals2.p, n, child.p, ibox.p, lbox.p, d_nodes, d_ltris, node_base, leaf_base);
+  k_pack<<<nb, TB, 0, st>>>(d_tris, vals2.p, n, child.p, ibox.p, lbox.p, d_nodes, d_ltris, d_lxf, node_base, leaf_base);
   cudaStreamSynchronize(st);
   return node_base;
 }

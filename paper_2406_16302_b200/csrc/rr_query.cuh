@@ -25,6 +25,7 @@ enum { QT_CLOSEST = 0, QT_SEG = 1 };
 
 
 
+
 struct __align__(16) Query {
   float3 o, d;
   float tmax;            // QT_SEG: segment length L; QT_CLOSEST: unused
@@ -80,12 +81,23 @@ __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay
     } else {
       int li = ~node;
       if (COUNT) nt++;
-      const float4* tp = S.ltris + 3 * li;
-      float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
-      float t = tri_hit(r, a, b, c);
+      // unit-triangle test (Woop 2004): plane distance, then barycentrics u, v of the plane point
+      const float4* xp = S.lxf + 3 * li;
+      const float4 m2 = __ldg(xp + 2);
+      const float oz = m2.w + m2.x * r.o.x + m2.y * r.o.y + m2.z * r.o.z;
+      const float dz = m2.x * r.d.x + m2.y * r.d.y + m2.z * r.d.z;
+      const float t = -oz / dz;
       if (t > tmin && t < tmax) {
-        tmax = leaf(li, t, tmax, __float_as_int(a.w));
-        if (tmax < 0.0f) break;
+        const float4 m0 = __ldg(xp);
+        const float u = (m0.w + m0.x * r.o.x + m0.y * r.o.y + m0.z * r.o.z) + t * (m0.x * r.d.x + m0.y * r.d.y + m0.z * r.d.z);
+        if (u >= 0.0f && u <= 1.0f) {
+          const float4 m1 = __ldg(xp + 1);
+          const float v = (m1.w + m1.x * r.o.x + m1.y * r.o.y + m1.z * r.o.z) + t * (m1.x * r.d.x + m1.y * r.d.y + m1.z * r.d.z);
+          if (v >= 0.0f && u + v <= 1.0f) {
+            tmax = leaf(li, t, tmax, __float_as_int(__ldg(S.ltris + 3 * li).w));
+            if (tmax < 0.0f) break;
+          }
+        }
       }
     }
     if (sp == 0) break;
