@@ -177,6 +177,16 @@ rr_status rr_render_residual(rr_ctx* ctx, const rr_render_args* args, float* d_i
  * the result back (blocking).  Used for end-to-end timing through the public API. */
 rr_status rr_render_residual_host(rr_ctx* ctx, const rr_render_args* args, float* h_image_rgba);
 
+/* Primal image I^D(state) (Eq.1-2; state 0 = new, 1 = old) by unidirectional path
+ * tracing with next-event estimation and BSDF sampling combined by the balance heuristic, spp samples per
+ * pixel, paths of <= max_depth edges, Philox key `seed` (streams disjoint from the residual ones).  Writes
+ * (overwrites) d_image_rgba (H*W*4 fp32, device, channel 3 = 0); RR_COUNT_TRAVERSAL in `flags` counts node
+ * fetches into rr_stats.  The image a residual is added to: I_new = I_old + residual.
+ * Asynchronous on cuda_stream.  Errors: RR_E_INVALID (null image, spp = 0, max_depth out of 1..RR_MAX_DEPTH,
+ * state > 1), RR_E_STATE (before upload), RR_E_CUDA. */
+rr_status rr_render_primal(rr_ctx* ctx, uint32_t state, uint32_t spp, uint64_t seed, uint32_t max_depth,
+                           uint32_t flags, float* d_image_rgba, uint64_t cuda_stream);
+
 /* Counters of the last render (blocking: synchronises the context's device). */
 rr_status rr_get_stats(rr_ctx* ctx, rr_stats* out);
 

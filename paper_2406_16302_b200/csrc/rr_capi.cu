@@ -645,6 +645,21 @@ rr_status rr_render_residual(rr_ctx* c, const rr_render_args* a, float* d_image,
   return cuda_check(c, "render launch");
 }
 
+rr_status rr_render_primal(rr_ctx* c, uint32_t state, uint32_t spp, uint64_t seed, uint32_t max_depth, uint32_t flags,
+                           float* d_image, uint64_t stream) {
+  if (!c) return RR_E_INVALID;
+  if (!c->have_scene) return fail(c, RR_E_STATE, "render before scene upload");
+  if (!d_image || spp == 0 || state > 1 || max_depth < 1 || max_depth > RR_MAX_DEPTH)
+    return fail(c, RR_E_INVALID, "bad primal render arguments");
+  cudaSetDevice(c->device);
+  if (cuda_check(c, "before primal") != RR_OK) return RR_E_CUDA;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(d_image, 0, (size_t)c->cam.width * c->cam.height * 4 * sizeof(float), st);
+  cudaMemsetAsync(c->stats.p, 0, STAT_COUNT * sizeof(unsigned long long), st);
+  launch_primal(c->S, (int)state, seed, (int)max_depth, spp, d_image, c->stats.p, (flags & RR_COUNT_TRAVERSAL) != 0, st);
+  return cuda_check(c, "primal launch");
+}
+
 rr_status rr_render_residual_host(rr_ctx* c, const rr_render_args* a, float* h_image) {
   if (!c || !h_image) return fail(c, RR_E_INVALID, "null argument");
   if (!c->have_scene) return fail(c, RR_E_STATE, "render before scene upload");

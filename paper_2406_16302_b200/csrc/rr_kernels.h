@@ -37,6 +37,8 @@ struct KArgs {
 void launch_residual(const DevScene& S, const KArgs& A, int grid, cudaStream_t st);
 int residual_grid(bool bidir, uint64_t n);  // blocks of residual_block() threads for n sample slots
 int residual_block();
+void launch_primal(const DevScene& S, int F, uint64_t seed, int D, uint32_t spp, float* image,
+                   unsigned long long* stats, bool count, cudaStream_t st);
 void launch_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out, cudaStream_t st);
 void launch_trace(const DevScene& S, int F, uint32_t n, const float* rays, float* hits, cudaStream_t st);
 void launch_segment(const DevScene& S, uint32_t n, const float* segs, float* out, cudaStream_t st);

@@ -62,7 +62,7 @@ __device__ __forceinline__ PV hit_pv(const DevScene& S, const Hit& h, P3 o, floa
 }
 
 // area-uniform point on a triangle set (C3): first k with cdf[k] > u0; su = sqrt(u1); b0 = 1-su; b1 = u2 su
-__device__ PV sample_set(const DevScene& S, const uint32_t* tris, const float* cdf, int n, int F, float u0, float u1,
+__device__ inline PV sample_set(const DevScene& S, const uint32_t* tris, const float* cdf, int n, int F, float u0, float u1,
                          float u2) {
   int lo = 0, hi = n - 1;
   while (lo < hi) {
@@ -118,7 +118,7 @@ __device__ __forceinline__ float area_pdf(const DevScene& S, int F, const PV& pr
 // x[0] = E, x[k-1] = L; e[i] = crossings of edge (x_i, x_{i+1}) with sa measured from x_i, sb from x_{i+1}.
 // Computed as (f / p_T7) / (1 + sum_c p_c / p_T7).
 // ------------------------------------------------------------------------------------------------
-__device__ float3 path_value(const DevScene& S, const PV* x, const Cross* e, int k, int F, uint32_t mask) {
+__device__ inline float3 path_value(const DevScene& S, const PV* x, const Cross* e, int k, int F, uint32_t mask) {
   const float3 zero = f3(0.f, 0.f, 0.f);
   float3 d01 = sub3(x[1].p, x[0].p);
   float dd01 = dot3(d01, d01);
@@ -192,7 +192,7 @@ __device__ __forceinline__ void splat(Out& o, int pix, float3 t) {
   o.splats++;
   atomicAdd(reinterpret_cast<float4*>(o.A->image) + pix, make_float4(t.x, t.y, t.z, 0.0f));
 }
-__device__ void emit_record(Out& o, uint64_t i, int kind, int a, int b, int status, int reason, int pix_p, float3 tp,
+__device__ inline void emit_record(Out& o, uint64_t i, int kind, int a, int b, int status, int reason, int pix_p, float3 tp,
                             int pix_q, float3 tq, float R) {
   const KArgs& A = *o.A;
   if (status == ST_ACCEPTED) o.acc++;
@@ -230,7 +230,7 @@ __device__ void emit_record(Out& o, uint64_t i, int kind, int a, int b, int stat
   }
 }
 // terms of one connection pair and splat
-__device__ void finish(Out& o, uint64_t i, int kind, int a, int b, int status, int reason, int pix_p, float3 vp,
+__device__ inline void finish(Out& o, uint64_t i, int kind, int a, int b, int status, int reason, int pix_p, float3 vp,
                        int pix_q, float3 vq, float R) {
   const KArgs& A = *o.A;
   float3 tp, tq;

@@ -71,6 +71,7 @@ class rr_path_record(C.Structure):
 
 
 EXPORTS = ["rr_create", "rr_destroy", "rr_last_error", "rr_scene_upload", "rr_set_edit", "rr_render_residual",
+           "rr_render_primal",
            "rr_render_residual_host", "rr_get_stats", "rr_trace", "rr_segment", "rr_philox", "rr_dump_paths",
            "rr_last_timings"]
 
@@ -102,6 +103,7 @@ def lib() -> C.CDLL:
     L.rr_dump_paths.argtypes = [P, C.POINTER(rr_render_args), U32, U32, U64, U64, C.POINTER(rr_path_record), U64,
                                 C.POINTER(U64)]
     L.rr_last_timings.argtypes = [P, C.POINTER(C.c_float), U32]
+    L.rr_render_primal.argtypes = [P, U32, U32, U64, U32, U32, P, U64]
     for name in EXPORTS:
         if name not in ("rr_destroy", "rr_last_error"):
             getattr(L, name).restype = C.c_int

@@ -135,6 +135,21 @@ class Renderer:
                     "rr_render_residual")
         return image
 
+    def render_primal(self, state: int, spp: int, seed: int, max_depth: int, image=None, stream: Optional[int] = None,
+                      count_traversal: bool = False):
+        """Primal image I^D(state) (state 0 = new, 1 = old) into a torch float32 (H, W, 4) CUDA tensor."""
+        import torch
+        if image is None:
+            image = torch.empty((self.height, self.width, 4), dtype=torch.float32, device=f"cuda:{self.device}")
+        assert image.is_cuda and image.dtype == torch.float32 and image.is_contiguous()
+        assert tuple(image.shape) == (self.height, self.width, 4)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        flags = N.RR_COUNT_TRAVERSAL if count_traversal else 0
+        self._check(self._L.rr_render_primal(self.h, int(state), int(spp), int(seed), int(max_depth), flags,
+                                             image.data_ptr(), int(stream)), "rr_render_primal")
+        return image
+
     def render_sequence(self, frames, args, image=None, shard_index: int = 0, shard_count: int = 1):
         """Chained residuals of an animation (config 5): frame f applies the edit S_f -> S_f+1
         (`frames[f]`, a list of edits), renders its residual with seed args.seed + f and adds it to `image`,

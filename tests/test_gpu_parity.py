@@ -318,3 +318,21 @@ def test_invalid_arguments_are_refused(torch_cuda):
     e = dataclasses.replace(w.edits[0], new_xform=w.edits[0].new_xform * 1.5)
     with pytest.raises(RRError):
         r.set_edit([e])
+
+
+# ---------------------------------------------------------------- primal renderer
+@pytest.mark.parametrize("cfg,W,spp,D", [(1, 32, 64, 4), (2, 32, 16, 6)])
+def test_primal_image_matches_oracle(torch_cuda, cfg, W, spp, D):
+    """I^D(F) on the GPU against the oracle's NEE/BSDF-MIS primal renderer on the same Philox streams."""
+    torch = torch_cuda
+    w = S.load_config(cfg, width=W, height=W, spp=spp, max_depth=D)
+    r = _renderer(w)
+    o = _oracle(w)
+    for F in (0, 1):
+        g = r.render_primal(F, spp, 7, D)[..., :3].double().cpu().numpy()
+        torch.cuda.synchronize()
+        ref, _ = o.primal(F, 7, spp, D)
+        scale = np.abs(ref).max()
+        assert scale > 0
+        rmse = math.sqrt(((g - ref) ** 2).mean())
+        assert rmse <= 1e-3 * scale, (F, rmse, scale)

@@ -49,3 +49,17 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", txt).lower(), f
+
+
+def test_pfm_roundtrip(tmp_path):
+    import numpy as np
+    from paper_2406_16302_b200.io import read_pfm, write_pfm
+    rng = np.random.default_rng(3)
+    for shape in ((5, 7, 3), (4, 6)):
+        a = rng.normal(size=shape).astype(np.float32)
+        p = str(tmp_path / "x.pfm")
+        write_pfm(p, a)
+        assert np.array_equal(read_pfm(p), a)
+    rgba = rng.normal(size=(3, 2, 4)).astype(np.float32)
+    write_pfm(p, rgba)
+    assert np.array_equal(read_pfm(p), rgba[..., :3])
