@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <unordered_map>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -49,6 +51,9 @@ struct rr_ctx {
   bool ev_init = false;
 };
 
+#ifndef RR_GROUPED_KEYS
+#define RR_GROUPED_KEYS 1  // static BLAS sorted by object-grouped keys (object Morton, then triangle Morton)
+#endif
 #ifndef RR_LARGE_FRAC
 #define RR_LARGE_FRAC 0.05  // "large" static triangle: box diagonal > this fraction of the static scene's
 #endif
@@ -287,13 +292,86 @@ rr_status rr_scene_upload(rr_ctx* c, const rr_scene_desc* d) {
     c->lxf.alloc(3 * total_leaves);
     cudaStream_t st = 0;
     int node_base = 0, leaf_base = 0;
-    auto build = [&](const std::vector<uint32_t>& tl) {
+    // Object-grouped sort keys for a static BLAS: (30-bit Morton code of the object's centroid, 4-bit tie
+    // break among objects in the same cell, 27-bit Morton code of the triangle within its object's box), so
+    // the Karras tree splits between objects first and every object's triangles form their own subtrees
+    // (SAH-free).
+    auto grouped_keys = [&](const std::vector<uint32_t>& tl, std::vector<unsigned long long>& keys) {
+      std::unordered_map<uint32_t, int> slot;
+      std::vector<std::array<float, 6>> ob;  // per object: box lo, hi
+      std::vector<int> tob(tl.size());
+      for (size_t k = 0; k < tl.size(); ++k) {
+        uint32_t o = c->tri_obj[tl[k]];
+        auto it = slot.find(o);
+        int j;
+        if (it == slot.end()) {
+          j = (int)ob.size();
+          slot[o] = j;
+          ob.push_back({3e38f, 3e38f, 3e38f, -3e38f, -3e38f, -3e38f});
+        } else {
+          j = it->second;
+        }
+        tob[k] = j;
+        for (int v = 0; v < 3; ++v) {
+          const float4& p = tv[3ull * tl[k] + v];
+          const float q[3] = {p.x, p.y, p.z};
+          for (int a = 0; a < 3; ++a) {
+            ob[j][a] = std::min(ob[j][a], q[a]);
+            ob[j][3 + a] = std::max(ob[j][3 + a], q[a]);
+          }
+        }
+      }
+      float clo[3] = {3e38f, 3e38f, 3e38f}, chi[3] = {-3e38f, -3e38f, -3e38f};
+      for (auto& b : ob)
+        for (int a = 0; a < 3; ++a) {
+          float m = 0.5f * (b[a] + b[3 + a]);
+          clo[a] = std::min(clo[a], m);
+          chi[a] = std::max(chi[a], m);
+        }
+      auto spread = [](uint64_t v, int bits) {  // bit i -> bit 3i
+        uint64_t r = 0;
+        for (int i = 0; i < bits; ++i) r |= ((v >> i) & 1ull) << (3 * i);
+        return r;
+      };
+      auto quant = [](float x, float lo, float hi, int bits) {
+        float e = hi - lo;
+        double u = e > 0 ? ((double)x - lo) / e : 0.5;
+        double m = (double)((1u << bits) - 1);
+        return (uint64_t)std::min(m, std::max(0.0, u * (1u << bits)));
+      };
+      std::vector<std::pair<uint64_t, int>> om(ob.size());
+      for (size_t j = 0; j < ob.size(); ++j) {
+        uint64_t code = 0;
+        for (int a = 0; a < 3; ++a) code |= spread(quant(0.5f * (ob[j][a] + ob[j][3 + a]), clo[a], chi[a], 10), 10) << (2 - a);
+        om[j] = {code, (int)j};
+      }
+      std::sort(om.begin(), om.end());
+      std::vector<uint64_t> hi_key(ob.size());
+      for (size_t r = 0; r < om.size(); ++r) {
+        int tie = 0;
+        if (r > 0 && om[r].first == om[r - 1].first) tie = std::min<int>(15, (int)(hi_key[om[r - 1].second] & 15) + 1);
+        hi_key[om[r].second] = (om[r].first << 4) | (uint64_t)tie;
+      }
+      keys.resize(tl.size());
+      for (size_t k = 0; k < tl.size(); ++k) {
+        const auto& b = ob[tob[k]];
+        const float4 &p0 = tv[3ull * tl[k]], &p1 = tv[3ull * tl[k] + 1], &p2 = tv[3ull * tl[k] + 2];
+        const float cen[3] = {(p0.x + p1.x + p2.x) / 3.0f, (p0.y + p1.y + p2.y) / 3.0f, (p0.z + p1.z + p2.z) / 3.0f};
+        uint64_t local = 0;
+        for (int a = 0; a < 3; ++a) local |= spread(quant(cen[a], b[a], b[3 + a], 9), 9) << (2 - a);
+        keys[k] = (hi_key[tob[k]] << 27) | local;
+      }
+    };
+    auto build = [&](const std::vector<uint32_t>& tl, bool grouped = false) {
       std::vector<float4> tb(3 * tl.size());
       for (size_t k = 0; k < tl.size(); ++k)
         for (int v = 0; v < 3; ++v) tb[3 * k + v] = tv[3ull * tl[k] + v];
       DevBuf<float4> dt;
       dt.upload(tb.data(), tb.size());
-      int root = build_lbvh(dt.p, (int)tl.size(), c->nodes.p, c->ltris.p, c->lxf.p, node_base, leaf_base, st);
+      std::vector<unsigned long long> keys;
+      if (grouped && RR_GROUPED_KEYS) grouped_keys(tl, keys);
+      int root = build_lbvh(dt.p, (int)tl.size(), c->nodes.p, c->ltris.p, c->lxf.p, node_base, leaf_base, st,
+                            keys.empty() ? nullptr : keys.data());
       node_base += (int)std::max<size_t>(tl.size() - 1, 1);
       leaf_base += (int)tl.size();
       return root;
@@ -326,10 +404,10 @@ rr_status rr_scene_upload(rr_ctx* c, const rr_scene_desc* d) {
         (d > RR_LARGE_FRAC * sd ? large : small).push_back(t);
       }
       if (large.empty() || small.empty()) {
-        static_root = build(stris);
+        static_root = build(stris, true);
       } else {
         const int top = node_base++;  // the extra root, reserved in total_nodes
-        int rs = build(small), rl = build(large);
+        int rs = build(small, true), rl = build(large);
         float a0[3], b0[3], a1[3], b1[3];
         box_of(small, a0, b0);
         box_of(large, a1, b1);

@@ -45,6 +45,6 @@ struct DevBuf {
 };
 
 int build_lbvh(const float4* d_tris, int n, float4* d_nodes, float4* d_ltris, float4* d_lxf, int node_base,
-               int leaf_base, cudaStream_t st);
+               int leaf_base, cudaStream_t st, const unsigned long long* h_keys = nullptr);
 
 }  // namespace rr

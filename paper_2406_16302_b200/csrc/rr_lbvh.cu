@@ -5,6 +5,8 @@
 // Replaces the paper's Embree BVH.
 #include <cub/cub.cuh>
 
+#include <vector>
+
 #include "rr_device.cuh"
 #include "rr_internal.h"
 
@@ -239,9 +241,10 @@ __global__ void k_pack(const float4* __restrict__ tris, const uint32_t* __restri
 }
 
 // Build one BLAS over n >= 1 triangles (3 float4 each, device).  Writes max(n-1,1) nodes at node_base and n
-// leaf triangles at leaf_base.  Returns the root node index (node_base).
+// leaf triangles at leaf_base.  Returns the root node index (node_base).  h_keys (optional, host, n): sort
+// keys to use instead of the triangles' own Morton codes (object-grouped keys, rr_capi.cu).
 int build_lbvh(const float4* d_tris, int n, float4* d_nodes, float4* d_ltris, float4* d_lxf, int node_base,
-               int leaf_base, cudaStream_t st) {
+               int leaf_base, cudaStream_t st, const unsigned long long* h_keys) {
   const int TB = 256;
   int nb = (n + TB - 1) / TB;
   int nred = nb < 1024 ? nb : 1024;
@@ -250,8 +253,16 @@ int build_lbvh(const float4* d_tris, int n, float4* d_nodes, float4* d_ltris, fl
   DevBuf<uint32_t> vals(n), vals2(n);
   DevBuf<int> child(2 * (n > 1 ? n - 1 : 1)), pint(n > 1 ? n - 1 : 1), pleaf(n), counter(n > 1 ? n - 1 : 1);
   DevBuf<Box> ibox(n > 1 ? n - 1 : 1), lbox(n);
-  k_centroid_bounds<<<nred, TB, 0, st>>>(d_tris, n, partial.p);
-  k_morton<<<nb, TB, 0, st>>>(d_tris, n, partial.p, nred, keys.p, vals.p);
+  if (h_keys && sizeof(MortonKey) == sizeof(unsigned long long)) {
+    std::vector<uint32_t> iota(n);
+    for (int k = 0; k < n; ++k) iota[k] = (uint32_t)k;
+    cudaMemcpyAsync(keys.p, h_keys, n * sizeof(MortonKey), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(vals.p, iota.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice, st);
+    cudaStreamSynchronize(st);
+  } else {
+    k_centroid_bounds<<<nred, TB, 0, st>>>(d_tris, n, partial.p);
+    k_morton<<<nb, TB, 0, st>>>(d_tris, n, partial.p, nred, keys.p, vals.p);
+  }
   size_t tmp_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys.p, keys2.p, vals.p, vals2.p, n, 0, RR_MORTON_BITS, st);
   DevBuf<char> tmp(tmp_bytes);

@@ -8,7 +8,7 @@ if [ "${NCU:-1}" = "1" ]; then
 timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
 echo "ncu launch list exit $?"
-timeout 1800 ncu --set full --clock-control none --import-source on -k regex:k_residual_bidir -c 1 \
-  -o gpurun_out/prof_full_t6 -f python tools/profile_run.py 4 1024 0x60 > gpurun_out/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_residual_bidir -c 1 \
+  -o gpurun_out/prof_full_t6 -f python tools/profile_run.py 4 512 0x60 8 > gpurun_out/ncu_full.log 2>&1
 echo "ncu full exit $?"
 fi
