@@ -113,6 +113,9 @@ typedef struct {
   float alpha_min;         /* roughness threshold, 0.1 */
   float dmin_rel;          /* distance threshold / scene diagonal, 0.01 */
   uint32_t shard_index, shard_count; /* sample-index sharding: blocks of 2^16 indices, block-cyclic */
+  uint32_t layer_mask;     /* techniques whose samples are rendered (bit l-1; 0 = all of technique_mask).  MIS
+                              weights still use technique_mask, so the per-technique layers of one mask add up
+                              to its full estimate (Fig. importance_sample rows B/C) */
 } rr_render_args;
 
 typedef struct {

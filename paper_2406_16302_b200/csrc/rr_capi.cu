@@ -710,6 +710,7 @@ rr_status rr_render_residual(rr_ctx* c, const rr_render_args* a, float* d_image,
   int sides = (a->flags & RR_TWO_WAY) ? 2 : 1;
   for (int l = 1; l <= 7; ++l) {
     if (!((mask >> (l - 1)) & 1u)) continue;
+    if (a->layer_mask && !((a->layer_mask >> (l - 1)) & 1u)) continue;  // per-technique layer
     for (int side = 0; side < sides; ++side) {
       KArgs K = make_kargs(c, a, mask, l, side);
       K.image = d_image;

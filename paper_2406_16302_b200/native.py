@@ -45,7 +45,7 @@ class rr_render_args(C.Structure):
     _fields_ = [("spp", C.c_uint32), ("seed", C.c_uint64), ("max_depth", C.c_uint32),
                 ("technique_mask", C.c_uint32), ("flags", C.c_uint32), ("jacobian_max", C.c_float),
                 ("alpha_min", C.c_float), ("dmin_rel", C.c_float), ("shard_index", C.c_uint32),
-                ("shard_count", C.c_uint32)]
+                ("shard_count", C.c_uint32), ("layer_mask", C.c_uint32)]
 
 
 class rr_stats(C.Structure):

@@ -113,6 +113,7 @@ class Renderer:
         r.technique_mask, r.flags = int(a.technique_mask), int(a.flags)
         r.jacobian_max, r.alpha_min, r.dmin_rel = float(a.jacobian_max), float(a.alpha_min), float(a.dmin_rel)
         r.shard_index, r.shard_count = int(shard_index), int(shard_count)
+        r.layer_mask = int(getattr(a, "layer_mask", 0))
         return r
 
     def render_residual(self, args, image=None, stream: Optional[int] = None, shard_index: int = 0,
@@ -149,6 +150,17 @@ class Renderer:
         self._check(self._L.rr_render_primal(self.h, int(state), int(spp), int(seed), int(max_depth), flags,
                                              image.data_ptr(), int(stream)), "rr_render_primal")
         return image
+
+    def render_layers(self, args) -> dict:
+        """Per-technique residual layers {l: (H, W, 4) CUDA tensor}: the samples of technique l only, MIS-weighted
+        against every technique of args.technique_mask; the layers add up to render_residual(args).  A technique
+        the library auto-disables (T4-T6 without a moved object) gives a zero layer."""
+        import dataclasses
+        out = {}
+        for l in range(1, 8):
+            if (int(args.technique_mask) >> (l - 1)) & 1:
+                out[l] = self.render_residual(dataclasses.replace(args, layer_mask=1 << (l - 1))).clone()
+        return out
 
     def render_sequence(self, frames, args, image=None, shard_index: int = 0, shard_count: int = 1):
         """Chained residuals of an animation (config 5): frame f applies the edit S_f -> S_f+1

@@ -109,6 +109,7 @@ class RenderArgs:
     jacobian_max: float = 10.0
     alpha_min: float = 0.1
     dmin_rel: float = 0.01       # SPEC.md L416 (x scene diagonal)
+    layer_mask: int = 0          # GPU only: render the samples of these techniques (0 = all); see rr.h
 
 
 @dataclasses.dataclass

@@ -336,3 +336,19 @@ def test_primal_image_matches_oracle(torch_cuda, cfg, W, spp, D):
         assert scale > 0
         rmse = math.sqrt(((g - ref) ** 2).mean())
         assert rmse <= 1e-3 * scale, (F, rmse, scale)
+
+
+def test_technique_layers_sum_to_full_render(torch_cuda):
+    """Per-technique layers (Fig. importance_sample rows B/C) add up to the
+    full residual, and each layer's records are those of its technique."""
+    torch = torch_cuda
+    w = S.config1(32, 32, spp=8, max_depth=4)
+    r = _renderer(w)
+    full = r.render_residual(w.args).clone()
+    layers = r.render_layers(w.args)
+    assert sorted(layers) == [1, 2, 3, 4, 5, 6, 7]
+    acc = sum(layers.values())
+    torch.cuda.synchronize()
+    scale = float(full.abs().max())
+    assert scale > 0 and all(float(x.abs().max()) > 0 for x in layers.values())
+    assert float((acc - full).abs().max()) <= 1e-5 * scale
