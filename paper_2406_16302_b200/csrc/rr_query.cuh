@@ -26,6 +26,7 @@ enum { QT_CLOSEST = 0, QT_SEG = 1 };
 
 
 
+
 struct __align__(16) Query {
   float3 o, d;
   float tmax;            // QT_SEG: segment length L; QT_CLOSEST: unused
@@ -86,7 +87,7 @@ __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay
       const float4 m2 = __ldg(xp + 2);
       const float oz = m2.w + m2.x * r.o.x + m2.y * r.o.y + m2.z * r.o.z;
       const float dz = m2.x * r.d.x + m2.y * r.d.y + m2.z * r.d.z;
-      const float t = -oz / dz;
+      const float t = __fdividef(-oz, dz);  // 2 ulp; the hit point itself is recomputed in fp64 (hit_pv)
       if (t > tmin && t < tmax) {
         const float4 m0 = __ldg(xp);
         const float u = (m0.w + m0.x * r.o.x + m0.y * r.o.y + m0.z * r.o.z) + t * (m0.x * r.d.x + m0.y * r.d.y + m0.z * r.d.z);
