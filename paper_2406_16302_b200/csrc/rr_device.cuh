@@ -265,11 +265,16 @@ __device__ __forceinline__ int project(const DevScene& S, P3 x) {
 struct WRay {
   float3 o, d, inv;
 };
+// reciprocal direction for the slab tests: the fast (2-ulp, no slow path) reciprocal is inside the tests'
+// conservative margin (box2: 1.0000004)
+__device__ __forceinline__ float3 rcp3(float3 d) {
+  return f3(__fdividef(1.0f, d.x), __fdividef(1.0f, d.y), __fdividef(1.0f, d.z));
+}
 __device__ __forceinline__ WRay make_wray(float3 o, float3 d) {
   WRay r;
   r.o = o;
   r.d = d;
-  r.inv = f3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
+  r.inv = rcp3(d);
   return r;
 }
 __device__ __forceinline__ void box2(const WRay& r, float4 n0, float4 n1, float4 n2, float tmin, float tmax,

@@ -156,7 +156,7 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
       const DevInstance& I = S.inst[k];
       place = kind == 1 ? F : 1 - F;
       tmax = kind == 1 ? best_t[F] : (seg ? L - S.eps : best_t[F] - S.eps);
-      float3 inv = f3(1.0f / d.x, 1.0f / d.y, 1.0f / d.z);
+      float3 inv = rcp3(d);
       if (!inst_box(I, place, o, inv, tmin, tmax)) continue;
       o = xf_point(I.Mi[place], q.o);
       d = xf_vec(I.Mi[place], q.d);
