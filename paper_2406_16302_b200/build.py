@@ -13,8 +13,11 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fma
          "-shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 
+STAMP = LIB + ".flags"
+
+
 def _stale() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(STAMP) or open(STAMP).read() != " ".join(FLAGS):
         return True
     t = os.path.getmtime(LIB)
     deps = SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.h*")) + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(HERE, "..", "include", "rr.h")]
@@ -33,6 +36,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         with open(os.path.join(HERE, "csrc", "ptxas_info.txt"), "w") as f:
             f.write(r.stderr)
         os.replace(tmp, LIB)
+        with open(STAMP, "w") as f:
+            f.write(" ".join(FLAGS))
     return LIB
 
 

@@ -85,15 +85,18 @@ __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay
       // unit-triangle test (Woop 2004): plane distance, then barycentrics u, v of the plane point
       const float4* xp = S.lxf + 3 * li;
       const float4 m2 = __ldg(xp + 2);
-      const float oz = m2.w + m2.x * r.o.x + m2.y * r.o.y + m2.z * r.o.z;
-      const float dz = m2.x * r.d.x + m2.y * r.d.y + m2.z * r.d.z;
+      // explicit FMAs (the library builds with -fmad=false; rounding here is the same for both states)
+      const float oz = fmaf(m2.x, r.o.x, fmaf(m2.y, r.o.y, fmaf(m2.z, r.o.z, m2.w)));
+      const float dz = fmaf(m2.x, r.d.x, fmaf(m2.y, r.d.y, m2.z * r.d.z));
       const float t = __fdividef(-oz, dz);  // 2 ulp; the hit point itself is recomputed in fp64 (hit_pv)
       if (t > tmin && t < tmax) {
         const float4 m0 = __ldg(xp);
-        const float u = (m0.w + m0.x * r.o.x + m0.y * r.o.y + m0.z * r.o.z) + t * (m0.x * r.d.x + m0.y * r.d.y + m0.z * r.d.z);
+        const float u = fmaf(t, fmaf(m0.x, r.d.x, fmaf(m0.y, r.d.y, m0.z * r.d.z)),
+                             fmaf(m0.x, r.o.x, fmaf(m0.y, r.o.y, fmaf(m0.z, r.o.z, m0.w))));
         if (u >= 0.0f && u <= 1.0f) {
           const float4 m1 = __ldg(xp + 1);
-          const float v = (m1.w + m1.x * r.o.x + m1.y * r.o.y + m1.z * r.o.z) + t * (m1.x * r.d.x + m1.y * r.d.y + m1.z * r.d.z);
+          const float v = fmaf(t, fmaf(m1.x, r.d.x, fmaf(m1.y, r.d.y, m1.z * r.d.z)),
+                               fmaf(m1.x, r.o.x, fmaf(m1.y, r.o.y, fmaf(m1.z, r.o.z, m1.w))));
           if (v >= 0.0f && u + v <= 1.0f) {
             tmax = leaf(li, t, tmax, __float_as_int(__ldg(S.ltris + 3 * li).w));
             if (tmax < 0.0f) break;
