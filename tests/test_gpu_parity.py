@@ -352,3 +352,16 @@ def test_technique_layers_sum_to_full_render(torch_cuda):
     scale = float(full.abs().max())
     assert scale > 0 and all(float(x.abs().max()) > 0 for x in layers.values())
     assert float((acc - full).abs().max()) <= 1e-5 * scale
+
+
+def test_equal_budget_ordering_config1(torch_cuda):
+    """The paper's claim at equal time: for a localized edit the residual estimator beats the
+    difference of two independent path-traced images."""
+    from paper_2406_16302_b200 import quality as Q
+    w = S.config1(64, 64, spp=8, max_depth=4)
+    r = _renderer(w)
+    ref = Q.reference(r, w.args, spp=1024)
+    res = Q.compare(r, w.args, 16, ref)
+    assert all(v["mse"] > 0 for v in res.values())
+    assert res["residual"]["efficiency"] > res["pt_difference"]["efficiency"], res
+    assert res["residual"]["mse"] < res["correlated_pt"]["mse"], res
