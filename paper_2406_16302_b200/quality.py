@@ -31,8 +31,9 @@ def _timed(fn):
 
 def reference(r, args, spp: int = 1024, seed: int = 1 << 20) -> np.ndarray:
     """High-sample residual (all techniques, two-way) on seeds disjoint from every estimator below.  Unbiased
-    (record-level parity with the oracle, whose residual converges to I(new) - I(old) in the oracle tests), and
-    its variance is far below a path-traced difference of the same spp, which would dominate every MSE."""
+    (record-level parity with the CPU reference implementation, whose residual converges to I(new) - I(old) in
+    its tests), and its variance is far below a path-traced difference of the same spp, which would dominate
+    every MSE."""
     a = dataclasses.replace(args, spp=spp + (spp & 1), seed=seed, flags=PAPER_FLAGS)
     img, _ = _timed(lambda: r.render_residual(a).clone())
     return img
