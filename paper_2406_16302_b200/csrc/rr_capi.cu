@@ -54,6 +54,9 @@ struct rr_ctx {
 #ifndef RR_GROUPED_KEYS
 #define RR_GROUPED_KEYS 1  // static BLAS sorted by object-grouped keys (object Morton, then triangle Morton)
 #endif
+#ifndef RR_CUBIC_KEYS
+#define RR_CUBIC_KEYS 1  // Morton keys over cubic cells (largest extent on every axis)
+#endif
 #ifndef RR_LARGE_FRAC
 #define RR_LARGE_FRAC 0.05  // "large" static triangle: box diagonal > this fraction of the static scene's
 #endif
@@ -339,10 +342,14 @@ rr_status rr_scene_upload(rr_ctx* c, const rr_scene_desc* d) {
         double m = (double)((1u << bits) - 1);
         return (uint64_t)std::min(m, std::max(0.0, u * (1u << bits)));
       };
+      float cext[3], cmax = 0.0f;  // cubic cells (RR_CUBIC_KEYS): split where the extent is largest
+      for (int a = 0; a < 3; ++a) cmax = std::max(cmax, chi[a] - clo[a]);
+      for (int a = 0; a < 3; ++a) cext[a] = RR_CUBIC_KEYS ? cmax : chi[a] - clo[a];
       std::vector<std::pair<uint64_t, int>> om(ob.size());
       for (size_t j = 0; j < ob.size(); ++j) {
         uint64_t code = 0;
-        for (int a = 0; a < 3; ++a) code |= spread(quant(0.5f * (ob[j][a] + ob[j][3 + a]), clo[a], chi[a], 10), 10) << (2 - a);
+        for (int a = 0; a < 3; ++a)
+          code |= spread(quant(0.5f * (ob[j][a] + ob[j][3 + a]), clo[a], clo[a] + cext[a], 10), 10) << (2 - a);
         om[j] = {code, (int)j};
       }
       std::sort(om.begin(), om.end());
@@ -358,7 +365,10 @@ rr_status rr_scene_upload(rr_ctx* c, const rr_scene_desc* d) {
         const float4 &p0 = tv[3ull * tl[k]], &p1 = tv[3ull * tl[k] + 1], &p2 = tv[3ull * tl[k] + 2];
         const float cen[3] = {(p0.x + p1.x + p2.x) / 3.0f, (p0.y + p1.y + p2.y) / 3.0f, (p0.z + p1.z + p2.z) / 3.0f};
         uint64_t local = 0;
-        for (int a = 0; a < 3; ++a) local |= spread(quant(cen[a], b[a], b[3 + a], 9), 9) << (2 - a);
+        float lext = 0.0f;
+        for (int a = 0; a < 3; ++a) lext = RR_CUBIC_KEYS ? std::max(lext, b[3 + a] - b[a]) : 0.0f;
+        for (int a = 0; a < 3; ++a)
+          local |= spread(quant(cen[a], b[a], b[a] + (RR_CUBIC_KEYS ? lext : b[3 + a] - b[a]), 9), 9) << (2 - a);
         keys[k] = (hi_key[tob[k]] << 27) | local;
       }
     };

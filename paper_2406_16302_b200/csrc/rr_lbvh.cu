@@ -12,6 +12,9 @@
 
 namespace rr {
 
+#ifndef RR_CUBIC_KEYS
+#define RR_CUBIC_KEYS 1  // Morton codes over the centroid bounds' enclosing cube (cubic cells)
+#endif
 #ifndef RR_MORTON_BITS
 #define RR_MORTON_BITS 63  // 21 bits per axis (30: 10 bits per axis)
 #endif
@@ -96,8 +99,9 @@ __global__ void k_morton(const float4* __restrict__ tris, int n, const float* __
   float4 A = tris[3 * k], B = tris[3 * k + 1], C = tris[3 * k + 2];
   float c[3] = {(A.x + B.x + C.x) * (1.0f / 3.0f), (A.y + B.y + C.y) * (1.0f / 3.0f), (A.z + B.z + C.z) * (1.0f / 3.0f)};
   uint32_t q[3];
+  const float cube = fmaxf(fmaxf(hi[0] - lo[0], hi[1] - lo[1]), hi[2] - lo[2]);
   for (int a = 0; a < 3; ++a) {
-    float ext = hi[a] - lo[a];
+    float ext = RR_CUBIC_KEYS ? cube : hi[a] - lo[a];
     float u = ext > 0.0f ? (c[a] - lo[a]) / ext : 0.5f;
     q[a] = (uint32_t)fminf(fmaxf(u * (float)RR_MORTON_CELLS, 0.0f), (float)(RR_MORTON_CELLS - 1));
   }
