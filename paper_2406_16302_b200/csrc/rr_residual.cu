@@ -774,9 +774,6 @@ __device__ __forceinline__ uint64_t fetch_work(unsigned long long* counter, bool
 // site (rr_query.cuh).
 // ------------------------------------------------------------------------------------------------
 #define RR_BLOCK 128
-#ifndef RR_CLOSEST_FIRST
-#define RR_CLOSEST_FIRST 0
-#endif
 #ifndef RR_MIN_BLOCKS
 #define RR_MIN_BLOCKS 16  // resident blocks per SM requested from the register allocator (32 registers:
                           // latency hiding beats the spills)
@@ -844,26 +841,8 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
       sc[3] += total;
     }
     sc[4] += active;
-#if RR_CLOSEST_FIRST
-    // closest-hit queries first, then segments: the long closest-hit traversals of the lanes line up at the
-    // same loop index instead of behind a lane-dependent number of connection segments
-    uint64_t order = 0;  // 4 bits per slot
-    {
-      int w = 0;
-      for (int k = 0; k < B.n; ++k)
-        if (B.q[k].type == QT_CLOSEST) order |= (uint64_t)k << (4 * w++);
-      for (int k = 0; k < B.n; ++k)
-        if (B.q[k].type != QT_CLOSEST) order |= (uint64_t)k << (4 * w++);
-    }
-    for (int k = 0; k < nmax; ++k)
-      if (k < B.n) {
-        const int kk = (int)((order >> (4 * k)) & 15ull);
-        run_query<COUNT>(S, B.q[kk], B.r[kk], o.qc);
-      }
-#else
     for (int k = 0; k < nmax; ++k)
       if (k < B.n) run_query<COUNT>(S, B.q[k], B.r[k], o.qc);
-#endif
     if (active) {
       sc[2]++;
       bool go;
