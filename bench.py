@@ -313,19 +313,34 @@ def run_ours(a):
                 roofline["traffic_source"] = tr["source"]
         except Exception:
             pass
-    # ---- end to end through the public API with host buffers (one render per step)
-    e2e = None
-    if rank == 0 and world == 1:
-        host = np.zeros((c.height, c.width, 4), np.float32)
-        r.render_residual_host(args, out=host)  # warm
-        t1 = time.perf_counter()
-        for _ in range(a.e2e_steps):
-            r.set_edit(w.edits)                    # per-step inputs: the edit (host -> device)
-            r.render_residual_host(args, out=host)  # render + image copy device -> host
-        el = time.perf_counter() - t1
-        h2d = len(w.edits) * C_sizeof_edit() + C_sizeof_args()
-        e2e = {"value": total_samples * a.e2e_steps / el, "unit": "samples/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(host.nbytes)}
+    # ---- end to end through the public API with host buffers (one render per step): each rank uploads its
+    # per-step input (the edit), renders its shard into HOST memory (rr_render_residual_host), and for N > 1
+    # the host images are summed on rank 0 (pinned host -> device, the NCCL reduce, device -> host).  Time =
+    # max over ranks of the wall time of the loop.
+    host = np.zeros((c.height, c.width, 4), np.float32)
+    r.render_residual_host(args, out=host, shard_index=rank, shard_count=world)  # warm
+    dev_img = torch.empty((c.height, c.width, 4), dtype=torch.float32, device=dev) if world > 1 else None
+    pinned = torch.from_numpy(host).pin_memory() if world > 1 else None
+    if world > 1:
+        dist.barrier()
+    t1 = time.perf_counter()
+    for _ in range(a.e2e_steps):
+        r.set_edit(w.edits)                                                         # host -> device input
+        r.render_residual_host(args, out=host, shard_index=rank, shard_count=world)  # render + device -> host
+        if world > 1:
+            pinned.copy_(torch.from_numpy(host))
+            dev_img.copy_(pinned, non_blocking=True)
+            reduce_image(dev_img, dst=0)
+            if rank == 0:
+                pinned.copy_(dev_img)
+    torch.cuda.synchronize(dev)
+    el = torch.tensor([time.perf_counter() - t1], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    h2d = len(w.edits) * C_sizeof_edit() + C_sizeof_args() + (int(host.nbytes) if world > 1 else 0)
+    d2h = int(host.nbytes) * (2 if world > 1 and rank == 0 else 1)
+    e2e = {"value": total_samples * a.e2e_steps / float(el.item()), "unit": "samples/s",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
     # ---- CPU baseline (oracle) on the host cores, rank 0 at N = 1 only
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
