@@ -188,6 +188,14 @@ def test_records_config1_deep(torch_cuda):
     record_parity(w, w.args)
 
 
+@pytest.mark.parametrize("D", [1, 2, 3, 10])
+def test_records_depth_limits(torch_cuda, D):
+    """Degenerate and maximum path budgets: D = 1 (direct emission only), 2, 3 (the two-ended techniques need
+    D >= 3 / 4) and RR_MAX_DEPTH = 10."""
+    w = S.config1(24, 24, spp=4, max_depth=D)
+    record_parity(w, w.args)
+
+
 def test_records_config2_material_edit(torch_cuda):
     w = S.config2()  # 256x256, 16 spp, D = 6 (GGX alpha 0.5 -> 0.1 and Lambert 0.8 -> 0.3)
     record_parity(w, w.args, n_per=40000)
