@@ -648,6 +648,7 @@ static rr_status check_args(rr_ctx* c, const rr_render_args* a) {
   if (a->max_depth < 1 || a->max_depth > RR_MAX_DEPTH) return fail(c, RR_E_INVALID, "max_depth out of [1, 10]");
   if (!(a->technique_mask & 0x40u)) return fail(c, RR_E_INVALID, "technique mask must contain T7");
   if (a->technique_mask & ~0x7Fu) return fail(c, RR_E_INVALID, "unknown technique bits");
+  if (a->layer_mask & ~0x7Fu) return fail(c, RR_E_INVALID, "unknown layer bits");
   if (!(a->flags & RR_TWO_WAY) && (a->flags & (RR_RECONNECT | RR_REJECT_MULTI)))
     return fail(c, RR_E_INVALID, "RR_RECONNECT / RR_REJECT_MULTI require RR_TWO_WAY");
   if (a->shard_count == 0 || a->shard_index >= a->shard_count) return fail(c, RR_E_INVALID, "bad shard");

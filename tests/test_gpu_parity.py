@@ -320,9 +320,14 @@ def test_invalid_arguments_are_refused(torch_cuda):
     w = S.config1(16, 16)
     r = _renderer(w)
     for bad in (dict(technique_mask=0x3F), dict(spp=3), dict(max_depth=0), dict(max_depth=11),
-                dict(flags=S.RECONNECT)):
+                dict(flags=S.RECONNECT), dict(layer_mask=0x80)):
         with pytest.raises(RRError):
             r.render_residual(dataclasses.replace(w.args, **bad))
+    for bad in (dict(state=2), dict(spp=0), dict(max_depth=0), dict(max_depth=11)):
+        kw = dict(state=0, spp=4, seed=1, max_depth=4)
+        kw.update(bad)
+        with pytest.raises(RRError):
+            r.render_primal(**kw)
     e = dataclasses.replace(w.edits[0], new_xform=w.edits[0].new_xform * 1.5)
     with pytest.raises(RRError):
         r.set_edit([e])
