@@ -304,6 +304,12 @@ def run_ours(a):
                 "all_launches": {"algorithmic_bytes_per_step": 64.0 * nodes + 48.0 * tris,
                                  "kernel_ms_per_step": float(kt.item()),
                                  "achieved_gbs": (64.0 * nodes + 48.0 * tris) / (float(kt.item()) / 1e3) / 1e9}}
+    ncu = os.path.join(ROOT, "profiles", "ncu_t6_metrics.json")  # binding-resource counters
+    if os.path.exists(ncu):
+        try:
+            roofline["ncu"] = json.load(open(ncu)).get(f"config{a.config}_T{dom}")
+        except Exception:
+            pass
     prof = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(prof):
         try:
