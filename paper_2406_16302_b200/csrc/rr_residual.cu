@@ -191,12 +191,14 @@ __device__ void single_issue(const DevScene& S, const KArgs& A, SState& st, Batc
         st.has_conn = true;
         st.pixp = st.pc_ ? project(S, P.v[m].p) : -1;
         st.pixq = st.qc_ ? project(S, Q.v[m].p) : -1;
-        bool shared = st.pc_ && st.qc_ && same_pv(S, P.v[m], Q.v[m]);
+        // a vertex that projects outside the image has a zero-valued sensor connection (reading 4): no query
+        const bool tp = st.pc_ && st.pixp >= 0, tq = st.qc_ && st.pixq >= 0;
+        bool shared = tp && tq && same_pv(S, P.v[m], Q.v[m]);
         if (shared) {
           st.q_cp = st.q_cq = B.push(mk_seg(P.v[m].p, E.p, P.v[m].tri, -1, 3));
         } else {
-          if (st.pc_) st.q_cp = B.push(mk_seg(P.v[m].p, E.p, P.v[m].tri, -1, bit(F)));
-          if (st.qc_) st.q_cq = B.push(mk_seg(Q.v[m].p, E.p, Q.v[m].tri, -1, bit(Fb)));
+          if (tp) st.q_cp = B.push(mk_seg(P.v[m].p, E.p, P.v[m].tri, -1, bit(F)));
+          if (tq) st.q_cq = B.push(mk_seg(Q.v[m].p, E.p, Q.v[m].tri, -1, bit(Fb)));
         }
       }
     }
@@ -300,14 +302,14 @@ __device__ bool single_consume(const DevScene& S, const KArgs& A, SState& st, co
     } else {
       pixp = st.pixp;
       pixq = st.pixq;
-      if (st.pc_ && B.r[st.q_cp].ok[F]) {
+      if (st.pc_ && st.q_cp >= 0 && B.r[st.q_cp].ok[F]) {
         x[0] = E;
         ce[0] = swapc(B.r[st.q_cp].c[F]);
         for (int j = 1; j <= m; ++j) { x[j] = P.v[m + 1 - j]; ce[j] = swapc(P.ex[m + 1 - j]); }
         x[m + 1] = P.v[0];
         vp = path_value(S, x, ce, m + 2, F, A.mask);
       }
-      if (qc_ && B.r[st.q_cq].ok[Fb]) {
+      if (qc_ && st.q_cq >= 0 && B.r[st.q_cq].ok[Fb]) {
         x[0] = E;
         ce[0] = swapc(B.r[st.q_cq].c[Fb]);
         for (int j = 1; j <= m; ++j) { x[j] = Q.v[m + 1 - j]; ce[j] = swapc(Q.ex[m + 1 - j]); }
@@ -575,7 +577,13 @@ __device__ void bidir_issue(const DevScene& S, const KArgs& A, int tech, int F, 
       int t = W.nconn + 1;
       const PV& v = W.v[t];
       if (side == 0) {
-        W.qc = B.push(mk_seg(v.p, E.p, v.tri, -1, bit(F)));
+        if (project(S, v.p) < 0) {  // the sensor connection cannot reach the image: value 0 (reading 4)
+          W.vis[t] = 0;
+          W.cc[t] = cross_zero();
+          W.nconn = t;
+        } else {
+          W.qc = B.push(mk_seg(v.p, E.p, v.tri, -1, bit(F)));
+        }
       } else {
         float d[8];
         rng.dims((uint32_t)(16 + t), d);
