@@ -30,7 +30,6 @@ __host__ __device__ __forceinline__ float dot3(float3 a, float3 b) { return a.x 
 __host__ __device__ __forceinline__ float3 cross3(float3 a, float3 b) {
   return f3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
 }
-__device__ __forceinline__ float3 norm3(float3 a) { return a * rsqrtf(dot3(a, a)); }
 __device__ __forceinline__ float3 norm3_exact(float3 a) { return a * (1.0f / sqrtf(dot3(a, a))); }
 __device__ __forceinline__ bool eq3(float3 a, float3 b) {
   return __float_as_uint(a.x) == __float_as_uint(b.x) && __float_as_uint(a.y) == __float_as_uint(b.y) &&
