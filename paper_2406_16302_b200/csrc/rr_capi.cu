@@ -34,6 +34,7 @@ struct rr_ctx {
   std::vector<int> dyn_objects;  // dynamic object ids in order (instance k -> object)
   std::vector<int> obj_inst;
   std::vector<int> inst_root;
+  int bvh_depth = 0;               // deepest root-to-leaf path over all BLAS roots, in inner nodes
   std::vector<float> inst_bbox;   // 6 per instance, object space
   // device buffers
   DevBuf<float4> nodes, ltris, lxf, tverts, mat, obj_emit;
@@ -445,6 +446,34 @@ rr_status rr_scene_upload(rr_ctx* c, const rr_scene_desc* d) {
       for (int a = 0; a < 3; ++a) c->inst_bbox.push_back(bh[a]);
     }
     if (cuda_check(c, "lbvh build") != RR_OK) return RR_E_CUDA;
+    // ---- traversal-stack bound: traverse() pushes at most one child per inner node on the path, so a tree
+    // deeper than RR_STACK inner nodes could drop subtrees; refuse it instead (Morton ties of 61-bit keys
+    // keep real scenes far below: config 4 measures 36, config 3 28).
+    if (node_base > 0) {
+      std::vector<int2> kids((size_t)node_base);
+      if (cudaMemcpy2D(kids.data(), sizeof(int2), reinterpret_cast<const char*>(c->nodes.p) + 3 * sizeof(float4),
+                       4 * sizeof(float4), sizeof(int2), (size_t)node_base, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return cuda_check(c, "bvh depth check");
+      std::vector<int> roots(c->inst_root);
+      roots.push_back(static_root);
+      int depth = 0;
+      std::vector<std::pair<int, int>> todo;
+      for (int r : roots) {
+        todo.assign(1, {r, 0});
+        while (!todo.empty()) {
+          auto [n, d] = todo.back();
+          todo.pop_back();
+          if (n < 0) continue;
+          depth = std::max(depth, d + 1);
+          if (d + 1 > RR_STACK || n >= node_base) break;
+          todo.push_back({kids[n].x, d + 1});
+          todo.push_back({kids[n].y, d + 1});
+        }
+      }
+      c->bvh_depth = depth;
+      if (depth > RR_STACK)
+        return fail(c, RR_E_INVALID, "scene BVH deeper than the traversal stack (" + std::to_string(RR_STACK) + ")");
+    }
     // ---- materials: scene materials + 2 slots (old, new) per dynamic object for edits
     c->obj_flags.upload(flags.data(), O);
     // ---- device scene
@@ -792,6 +821,7 @@ rr_status rr_get_stats(rr_ctx* c, rr_stats* out) {
   out->tris_tested = h[STAT_TRIS];
   for (int r = 0; r < 6; ++r) out->rejected_by[r] = h[STAT_REJBY + r];
   for (int r = 0; r < 8; ++r) out->sched[r] = h[STAT_SCHED + r];
+  out->sched[5] = (uint64_t)c->bvh_depth;
   out->effective_mask = c->last_mask;
   out->n_moved = 0;
   for (int k = 0; k < c->S.n_inst; ++k) out->n_moved += c->S.inst[k].moved ? 1 : 0;

@@ -121,6 +121,8 @@ def test_lbvh_closest_hit_matches_oracle(torch_cuda, cfg):
     w = S.load_config(cfg, width=16, height=16)
     r = _renderer(w)
     o = _oracle(w)
+    depth = r.get_stats()["sched"][5]  # deepest BLAS path; upload refuses trees deeper than the stack (64)
+    assert 0 < depth <= 64, depth
     rng = np.random.default_rng(cfg)
     n = 3000
     lo, hi = (np.array([0.02] * 3), np.array([0.98] * 3)) if cfg < 3 else (np.array([0.2, 0.05, 0.2]), np.array([9.8, 2.9, 9.8]))

@@ -37,6 +37,7 @@ for k in cfgs:
           f"GB/s(alg) {(64 * st['nodes_visited'] + 48 * st['tris_tested']) / ms / 1e6:.1f}", flush=True)
     sc = st["sched"]
     if sc[0]:
-        print(f"   sched: queries/round {sc[3] / sc[0]:.1f}, lanes holding {sc[4] / sc[0]:.1f}/32", flush=True)
+        print(f"   sched: queries/round {sc[3] / sc[0]:.1f}, lanes holding {sc[4] / sc[0]:.1f}/32, bvh depth {sc[5]}",
+              flush=True)
     print("   per launch ms:", [round(x, 2) for x in tm[1:15]], " img sum", img[..., :3].sum().item(), flush=True)
     del r
