@@ -13,6 +13,9 @@
 #define RR_PI_F 3.14159265358979323846f
 #define RR_INV_PI_F 0.318309886183790671538f
 #define RR_STACK 64
+#ifndef RR_SSTACK
+#define RR_SSTACK 0  // traversal-stack entries kept in shared memory (blocks of 128 threads); 0: all local
+#endif
 #define RR_TMAX 1.0e30f  // every query's tmax is below the 'empty child' sentinel box at 3e38
 
 namespace rr {

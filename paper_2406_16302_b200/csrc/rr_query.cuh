@@ -50,7 +50,15 @@ template <bool COUNT, class Leaf>
 __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay& r_in, float tmin, float tmax, Leaf leaf,
                                          TCount& tc) {
   const WRay& r = r_in;
+#if RR_SSTACK > 0
+  // short stack: the first RR_SSTACK entries in shared memory (entry k of thread t at [k][t], conflict-free),
+  // the rest in local memory
+  __shared__ int sstack[RR_SSTACK][128];
+  int* const sbase = &sstack[0][threadIdx.x];
+  int stack[RR_STACK - RR_SSTACK];
+#else
   int stack[RR_STACK];
+#endif
   int sp = 0;
   int node = root;
   uint32_t nn = 0, nt = 0;
@@ -69,7 +77,12 @@ __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay
           c0 = c1;
           c1 = t;
         }
+#if RR_SSTACK > 0
+        if (sp < RR_SSTACK) sbase[128 * sp++] = c1;
+        else if (sp < RR_STACK) { stack[sp - RR_SSTACK] = c1; sp++; }
+#else
         if (sp < RR_STACK) stack[sp++] = c1;
+#endif
         node = c0;
         continue;
       } else if (h0) {
@@ -105,7 +118,12 @@ __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay
       }
     }
     if (sp == 0) break;
+#if RR_SSTACK > 0
+    --sp;
+    node = sp < RR_SSTACK ? sbase[128 * sp] : stack[sp - RR_SSTACK];
+#else
     node = stack[--sp];
+#endif
   }
   tc.nodes += nn;
   tc.tris += nt;
