@@ -4,9 +4,13 @@ Estimators of the residual Delta = I(new) - I(old) compared against a high-sampl
   * "pt_difference"   -- path tracing from scratch in each state with independent seeds (P:L504-506);
   * "correlated_pt"   -- camera paths only (T7), random-number replay in both states (mask {7}, one-way;
                          P:L510-511);
-  * "residual"        -- the paper's method: all seven techniques, path mapping, two-way.
-Each is timed with CUDA events on the device; mse() is taken against the reference and efficiency =
-1 / (mse * seconds).  Scenes are the synthetic stand-ins of rr_inputs (no measured data).
+  * "residual"        -- the paper's method: all seven techniques, path mapping, two-way (P:L285-436);
+ablations of the method (the mapping components of P:L387-436, one at a time):
+  * "residual_replay" -- two-way, no reconnection: diverged paths are replayed only (RR_RECONNECT off);
+  * "residual_one_way"-- one side per technique, replay only (flags 0; SPEC's "mapping off" run knob).
+Each is timed with CUDA events on the device; mse() and ssim() are taken against the reference and
+efficiency = 1 / (mse * seconds).  Scenes are the synthetic stand-ins of rr_inputs (no
+measured data).
 """
 from __future__ import annotations
 
@@ -39,7 +43,7 @@ def reference(r, args, spp: int = 1024, seed: int = 1 << 20) -> np.ndarray:
     return img
 
 
-def estimators(r, args, spp: int, seed: int = 0) -> Dict[str, tuple]:
+def estimators(r, args, spp: int, seed: int = 0, ablations: bool = False) -> Dict[str, tuple]:
     """{name: (image, seconds)} at `spp` samples per pixel per technique (PT: spp per state)."""
     out = {}
     out["pt_difference"] = _timed(lambda: r.render_primal(0, spp, seed + 11, args.max_depth).clone()
@@ -48,6 +52,11 @@ def estimators(r, args, spp: int, seed: int = 0) -> Dict[str, tuple]:
     out["correlated_pt"] = _timed(lambda: r.render_residual(corr).clone())
     full = dataclasses.replace(args, spp=spp + (spp & 1), seed=seed + 14, flags=PAPER_FLAGS)
     out["residual"] = _timed(lambda: r.render_residual(full).clone())
+    if ablations:
+        rep = dataclasses.replace(full, seed=seed + 15, flags=PAPER_FLAGS & ~2)
+        out["residual_replay"] = _timed(lambda: r.render_residual(rep).clone())
+        one = dataclasses.replace(args, spp=spp, seed=seed + 16, flags=0)
+        out["residual_one_way"] = _timed(lambda: r.render_residual(one).clone())
     return out
 
 
@@ -55,9 +64,29 @@ def mse(img: np.ndarray, ref: np.ndarray) -> float:
     return float(((img - ref) ** 2).mean())
 
 
-def compare(r, args, spp: int, ref: np.ndarray, seed: int = 0) -> Dict[str, dict]:
+def _box(a: np.ndarray, k: int) -> np.ndarray:
+    """mean over every k x k window (valid positions only), via a summed-area table"""
+    c = np.pad(a, ((1, 0), (1, 0))).cumsum(0).cumsum(1)
+    return (c[k:, k:] - c[:-k, k:] - c[k:, :-k] + c[:-k, :-k]) / (k * k)
+
+
+def ssim(img: np.ndarray, ref: np.ndarray, k: int = 7) -> float:
+    """Mean structural similarity (Wang et al. 2004) of the channel-mean images, k x k uniform windows,
+    C1 = (0.01 L)^2, C2 = (0.03 L)^2 with L the reference's value range (residuals are signed)."""
+    x, y = img.mean(axis=-1), ref.mean(axis=-1)
+    L = float(y.max() - y.min()) or 1.0
+    c1, c2 = (0.01 * L) ** 2, (0.03 * L) ** 2
+    mx, my = _box(x, k), _box(y, k)
+    vx, vy, cxy = _box(x * x, k) - mx * mx, _box(y * y, k) - my * my, _box(x * y, k) - mx * my
+    s = ((2 * mx * my + c1) * (2 * cxy + c2)) / ((mx * mx + my * my + c1) * (vx + vy + c2))
+    return float(s.mean())
+
+
+def compare(r, args, spp: int, ref: np.ndarray, seed: int = 0, ablations: bool = False) -> Dict[str, dict]:
     res = {}
-    for name, (img, sec) in estimators(r, args, spp, seed).items():
+    estimators(r, args, spp, seed + 1000, ablations)  # warm-up: first launches of each kernel are not timed
+    for name, (img, sec) in estimators(r, args, spp, seed, ablations).items():
         m = mse(img, ref)
-        res[name] = {"mse": m, "seconds": sec, "efficiency": 1.0 / (m * sec) if m > 0 and sec > 0 else float("inf")}
+        res[name] = {"mse": m, "ssim": ssim(img, ref), "seconds": sec,
+                     "efficiency": 1.0 / (m * sec) if m > 0 and sec > 0 else float("inf")}
     return res

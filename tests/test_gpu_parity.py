@@ -380,3 +380,4 @@ def test_equal_budget_ordering_config1(torch_cuda):
     assert all(v["mse"] > 0 for v in res.values())
     assert res["residual"]["efficiency"] > res["pt_difference"]["efficiency"], res
     assert res["residual"]["mse"] < res["correlated_pt"]["mse"], res
+    assert res["residual"]["ssim"] > res["pt_difference"]["ssim"], res

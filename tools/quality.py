@@ -16,4 +16,4 @@ r.upload(w.scene)
 r.set_edit(w.edits)
 ref = Q.reference(r, w.args, ref_spp)
 print(json.dumps({"config": cfg, "resolution": W, "spp": spp, "reference_spp": ref_spp,
-                  "results": Q.compare(r, w.args, spp, ref)}, indent=1))
+                  "results": Q.compare(r, w.args, spp, ref, ablations=True)}, indent=1))
