@@ -185,6 +185,50 @@ def test_records_config1_full(torch_cuda, flags):
     record_parity(w, args)
 
 
+def test_stats_accounting_matches_oracle(torch_cuda):
+    """Per-technique diagnostics: every (technique, side) runs
+    N_pix * spp / 2 samples; every connection is accepted, rejected (by reason) or unpaired; the GPU's counters
+    agree with the oracle's record statuses over the same full sample range."""
+    torch = torch_cuda
+    w = S.config1()
+    r = _renderer(w)
+    o = _oracle(w)
+    r.render_residual(w.args)
+    torch.cuda.synchronize()
+    st = r.get_stats()
+    mask = o.effective_mask(w.args.technique_mask)
+    n_tech = bin(mask).count("1")
+    W, H = w.scene.camera.width, w.scene.camera.height
+    assert st["samples"] == n_tech * W * H * w.args.spp
+    assert st["mapped_only"] == 0
+    assert st["connections"] == st["accepted"] + st["rejected"] + st["unpaired"]
+    assert sum(st["rejected_by"]) == st["rejected"]
+    cnt = {"accepted": 0, "rejected": 0, "unpaired": 0}
+    by = [0] * 6
+    for l in range(1, 8):
+        if not (mask >> (l - 1)) & 1:
+            continue
+        for s in (0, 1):
+            _, recs, _ = o.residual(w.args, l, s, 0, o.sample_range(w.args), records=True)
+            for rec in recs:
+                k = ("accepted", "rejected", "unpaired")[int(rec.status)]
+                cnt[k] += 1
+                if rec.status == 1:
+                    by[int(rec.reason) if 0 <= rec.reason < 6 else 0] += 1
+    assert cnt["accepted"] > 0 and cnt["rejected"] > 0
+    for k, v in cnt.items():
+        assert abs(st[k] - v) <= max(2, 2e-3 * v), (k, st[k], v)
+    g = st["rejected_by"]
+    close = lambda a, b: abs(a - b) <= max(2, 2e-3 * b)  # noqa: E731
+    for q in (0, 3, 4, 5):  # none, multi, target, suffix-dynamic: same tests in the same order on both sides
+        assert close(g[q], by[q]), (q, g, by)
+    # a reconnection failing both the Jacobian bound and the visibility of its edge: the oracle tests the edge
+    # first (reason 1), the GPU tests the Jacobian before it spends a query on the edge (reason 2; DESIGN.md
+    # reading 11).  Same rejections, same contributions.
+    assert close(g[1] + g[2], by[1] + by[2]), (g, by)
+    assert g[2] >= by[2] - 2 and g[1] <= by[1] + 2, (g, by)
+
+
 def test_records_config1_deep(torch_cuda):
     w = S.config1(32, 32, spp=4, max_depth=8)
     record_parity(w, w.args)
