@@ -12,7 +12,9 @@
 //     explicit per-path pdf products (the "two tables" of P:L356 written out directly), the path mapping
 //     of Sec.5 (random-seed replay P:L414-416, object transform P:L381-385, dynamic<->ghost pair
 //     P:L418-420, keep-vertex reconnection with the Jacobian of P:L397-401 and criteria P:L403-411),
-//     rejection and two-way mapping.
+//     rejection and two-way mapping;
+//   * optionally (flags bit 32) GGX directions from the visible-normal distribution (Heitz 2018), one of
+//     the variance-only variants of SURVEY 8(f) row 4.
 // Where the paper is silent the reading of SURVEY.md 8(c) (C1-C12) is followed; DESIGN.md lists them.
 //
 // Every quantity is computed in double precision from the fp32 scene arrays.  The only fp32 data are
@@ -98,6 +100,7 @@ struct Mat {
   int type;
   V3 albedo;
   double alpha;
+  bool vndf = false;  // GGX directions sampled from the visible normals of wi (RR_VNDF)
 };
 struct Tri {
   V3 v0, v1, v2;
@@ -249,6 +252,7 @@ struct Scene {
   std::vector<double> xf[2];        // per object 12 doubles per state (F=0: new, F=1: old)
   std::vector<int> has_mat;
   std::vector<Mat> emat[2];
+  bool vndf = false;                // render option RR_VNDF (flags bit 32) of the current residual call
   // derived
   double diag, eps;
   V3 cf, cr, cu;  // camera basis
@@ -308,8 +312,9 @@ void build_set(const Scene& S, Scene::TriSet& ts) {
 }
 
 Mat mat_of(const Scene& S, int obj, int F) {
-  if (S.edited[obj] && S.has_mat[obj]) return S.emat[F][obj];
-  return S.mats[S.obj_mat[obj]];
+  Mat m = (S.edited[obj] && S.has_mat[obj]) ? S.emat[F][obj] : S.mats[S.obj_mat[obj]];
+  m.vndf = S.vndf && m.type == MAT_GGX;
+  return m;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -452,7 +457,33 @@ double bsdf_pdf(const Mat& m, V3 n, V3 wi, V3 wo) {
   if (m.type == MAT_LAMBERT) return co / PI;
   V3 h = normalize(wi + wo);
   double nh = dot(ns, h);
+  // VNDF (Heitz 2018): h has density D_wi(h) = G1(wi) max(0, wi.h) D(h) / (n.wi); with the reflection
+  // Jacobian 1 / (4 wo.h) and wo.h = wi.h this is G1(wi) D(h) / (4 n.wi)
+  if (m.vndf) return ggx_G1(m.alpha, ci) * ggx_D(m.alpha, nh) / (4.0 * ci);
   return ggx_D(m.alpha, nh) * std::fabs(nh) / (4.0 * std::fabs(dot(wo, h)));
+}
+// Visible-normal sample of the GGX distribution (Heitz 2018, "Sampling the GGX distribution of visible
+// normals", Listing 1), isotropic alpha, in the frame (b1, b2, ns) of local_to_world:
+//   1. stretch wi: Vh = normalize(a wi_x, a wi_y, wi_z);
+//   2. basis T1 = normalize(-Vh_y, Vh_x, 0) (e_x if Vh = e_z), T2 = Vh x T1;
+//   3. disk point (r cos phi, r sin phi), r = sqrt(u1), phi = 2 pi u2, its second coordinate warped to the
+//      projected hemisphere: t2 = (1 - s) sqrt(1 - t1^2) + s t2 with s = (1 + Vh_z) / 2;
+//   4. Nh = t1 T1 + t2 T2 + sqrt(max(0, 1 - t1^2 - t2^2)) Vh;
+//   5. unstretch: h = normalize(a Nh_x, a Nh_y, max(0, Nh_z)).
+V3 ggx_vndf_half(double a, V3 ns, V3 wi, double u1, double u2) {
+  V3 b1, b2;
+  onb(ns, b1, b2);
+  V3 vh = normalize(v3(a * dot(wi, b1), a * dot(wi, b2), dot(wi, ns)));
+  double lensq = vh.x * vh.x + vh.y * vh.y;
+  V3 t1v = lensq > 0 ? v3(-vh.y, vh.x, 0.0) * (1.0 / std::sqrt(lensq)) : v3(1.0, 0.0, 0.0);
+  V3 t2v = cross(vh, t1v);
+  double r = std::sqrt(u1), phi = 2.0 * PI * u2;
+  double t1 = r * std::cos(phi), t2 = r * std::sin(phi);
+  double sw = 0.5 * (1.0 + vh.z);
+  t2 = (1.0 - sw) * std::sqrt(1.0 - t1 * t1) + sw * t2;
+  V3 nh = t1v * t1 + t2v * t2 + vh * std::sqrt(std::max(0.0, 1.0 - t1 * t1 - t2 * t2));
+  V3 hl = normalize(v3(a * nh.x, a * nh.y, std::max(0.0, nh.z)));
+  return local_to_world(ns, hl.x, hl.y, hl.z);
 }
 bool bsdf_sample(const Mat& m, V3 n, V3 wi, double u1, double u2, V3& wo) {
   V3 ns = dot(n, wi) > 0 ? n : n * -1.0;
@@ -462,6 +493,13 @@ bool bsdf_sample(const Mat& m, V3 n, V3 wi, double u1, double u2, V3& wo) {
     return true;
   }
   double a = m.alpha;
+  if (m.vndf) {
+    V3 h = normalize(ggx_vndf_half(a, ns, wi, u1, u2));
+    wo = h * (2.0 * dot(wi, h)) - wi;
+    if (!(dot(wo, ns) > 0)) return false;
+    wo = normalize(wo);
+    return true;
+  }
   double tan2 = a * a * u1 / (1.0 - u1);
   double ct = 1.0 / std::sqrt(1.0 + tan2);
   double st = std::sqrt(std::max(0.0, 1.0 - ct * ct));
@@ -1087,7 +1125,7 @@ typedef struct {
   uint64_t seed;
   uint32_t max_depth;
   uint32_t technique_mask;
-  uint32_t flags;  // 1 TWO_WAY, 2 RECONNECT, 4 REJECT_MULTI
+  uint32_t flags;  // 1 TWO_WAY, 2 RECONNECT, 4 REJECT_MULTI, 32 VNDF (GGX visible-normal sampling)
   double jacobian_max, alpha_min, dmin_rel;
 } orc_args;
 
@@ -1618,6 +1656,7 @@ double orc_scene_diag(void* h) { return ((Oracle*)h)->S.diag; }
 int orc_residual(void* h, const orc_args* A, int tech, int side, uint64_t i0, uint64_t i1, double* img,
                  orc_record* recs, int64_t cap, int64_t* n_recs, orc_stats* stats) {
   Oracle* O = (Oracle*)h;
+  O->S.vndf = (A->flags & 32u) != 0;
   Ctx cx;
   cx.S = &O->S;
   cx.mask = effective_mask(O->S, A->technique_mask);
@@ -1644,6 +1683,7 @@ int orc_residual(void* h, const orc_args* A, int tech, int side, uint64_t i0, ui
 // Primal render of state F (0 = N, 1 = O): samples idx in [i0, i1) (pixel = idx mod N_pix).
 int orc_primal(void* h, int F, uint64_t seed, int D, uint64_t i0, uint64_t i1, double* img, orc_stats* stats) {
   Oracle* O = (Oracle*)h;
+  O->S.vndf = false;  // the primal renderer samples GGX from D(h) |n.h|
   Ctx cx;
   cx.S = &O->S;
   cx.mask = 0x7F;
@@ -1658,6 +1698,7 @@ int orc_primal(void* h, int F, uint64_t seed, int D, uint64_t i0, uint64_t i1, d
 // debug: print the base / mapped connection paths of one sample
 void orc_debug_sample(void* h, const orc_args* A, int tech, int side, uint64_t i) {
   Oracle* O = (Oracle*)h;
+  O->S.vndf = (A->flags & 32u) != 0;
   Ctx cx;
   cx.S = &O->S;
   cx.mask = effective_mask(O->S, A->technique_mask);
@@ -1745,7 +1786,8 @@ int orc_crossings_brute(void* h, int F, const double a[3], const double b[3]) {
 // BSDF: mat = {type, albedo r,g,b, alpha}; out_eval[3], returns pdf
 double orc_bsdf(const double mat[5], const double n[3], const double wi[3], const double wo[3], double out_eval[3]) {
   Mat m;
-  m.type = (int)mat[0];
+  m.type = (int)mat[0] == 2 ? MAT_GGX : (int)mat[0];  // 2: GGX with visible-normal sampling
+  m.vndf = (int)mat[0] == 2;
   m.albedo = v3(mat[1], mat[2], mat[3]);
   m.alpha = mat[4];
   V3 e = bsdf_eval(m, v3(n[0], n[1], n[2]), v3(wi[0], wi[1], wi[2]), v3(wo[0], wo[1], wo[2]));
@@ -1754,7 +1796,8 @@ double orc_bsdf(const double mat[5], const double n[3], const double wi[3], cons
 }
 int orc_bsdf_sample(const double mat[5], const double n[3], const double wi[3], double u1, double u2, double wo[3]) {
   Mat m;
-  m.type = (int)mat[0];
+  m.type = (int)mat[0] == 2 ? MAT_GGX : (int)mat[0];  // 2: GGX with visible-normal sampling
+  m.vndf = (int)mat[0] == 2;
   m.albedo = v3(mat[1], mat[2], mat[3]);
   m.alpha = mat[4];
   V3 w;

@@ -36,6 +36,7 @@ RECONNECT = 2
 REJECT_MULTI = 4
 ACCUMULATE = 8
 PAPER_FLAGS = TWO_WAY | RECONNECT | REJECT_MULTI
+VNDF = 32  # GGX directions from the visible normals (Heitz 2018), both implementations
 
 
 @dataclasses.dataclass

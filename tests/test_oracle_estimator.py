@@ -16,7 +16,7 @@ def _pool():
 
 
 # ---------------------------------------------------------------- exact special cases
-@pytest.mark.parametrize("flags", [S.PAPER_FLAGS, S.TWO_WAY, 0])
+@pytest.mark.parametrize("flags", [S.PAPER_FLAGS, S.TWO_WAY, 0, S.PAPER_FLAGS | S.VNDF])
 def test_identity_edit_is_exactly_zero(flags):
     """old_xform == new_xform bitwise and equal materials: every record cancels bitwise (S:L181,
     S:L507); the object stays dynamic so T1-T3 and T7 all run (no API short-circuit)."""
@@ -158,7 +158,8 @@ def test_material_edit_masks_agree():
     seeds = range(24)
     with _pool() as p:
         ref = np.stack(p.map(_render, [(2, 12, s, 0x40, S.TWO_WAY, 4) for s in seeds]))
-        for mask, flags in ((0x47, S.TWO_WAY), (0x47, S.PAPER_FLAGS), (0x41, S.PAPER_FLAGS), (0x44, S.TWO_WAY)):
+        for mask, flags in ((0x47, S.TWO_WAY), (0x47, S.PAPER_FLAGS), (0x41, S.PAPER_FLAGS), (0x44, S.TWO_WAY),
+                            (0x47, S.PAPER_FLAGS | S.VNDF), (0x44, S.TWO_WAY | S.VNDF), (0x40, S.VNDF)):
             other = np.stack(p.map(_render, [(2, 12, s, mask, flags, 4) for s in seeds]))
             _agree(ref, other, pix_frac=0.95)  # GGX alpha 0.1 light-tracing splats are heavy-tailed
 

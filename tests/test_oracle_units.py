@@ -99,7 +99,8 @@ def test_ggx_reciprocity(alpha):
         assert a == pytest.approx(b, rel=1e-12, abs=1e-300)
 
 
-@pytest.mark.parametrize("mat", [[0, 0.8, 0.8, 0.8, 1.0], [1, 1.0, 1.0, 1.0, 0.1], [1, 1.0, 1.0, 1.0, 0.6]])
+@pytest.mark.parametrize("mat", [[0, 0.8, 0.8, 0.8, 1.0], [1, 1.0, 1.0, 1.0, 0.1], [1, 1.0, 1.0, 1.0, 0.6],
+                                 [2, 1.0, 1.0, 1.0, 0.1], [2, 1.0, 1.0, 1.0, 0.6]])
 def test_sampling_density_matches_pdf(mat):
     """E[1/pdf(wo)] over valid samples = 2 pi iff the sampler's density equals pdf on the hemisphere;
     E[rho cos / pdf] <= 1 (energy)."""
@@ -121,6 +122,59 @@ def test_sampling_density_matches_pdf(mat):
         m, s = inv.mean(), inv.std() / math.sqrt(N)
         assert abs(m - 2 * math.pi) < 4 * s + 1e-3, (m, s)
         assert en.mean() < 1.0 + 3 * en.std() / math.sqrt(N)
+
+
+# ---------------------------------------------------------------- GGX visible-normal sampling
+def _g1(a, c):
+    """Smith G1 of GGX (Walter et al. 2007, Eq. 34 written with cos): 2 / (1 + sqrt(1 + a^2 tan^2))"""
+    return 2.0 / (1.0 + math.sqrt(1.0 + a * a * (1.0 - c * c) / (c * c)))
+
+
+@pytest.mark.parametrize("alpha", [0.1, 0.5, 1.0])
+def test_vndf_equals_ndf_sampling_at_normal_incidence(alpha):
+    """At wi = n the visible-normal distribution is D(h)(n.h) (G1(n) = 1), so Heitz's warp reduces to the
+    classic inversion tan^2 = a^2 u1 / (1 - u1): same direction for the same (u1, u2), same pdf."""
+    rng = np.random.default_rng(4)
+    n, wi = np.array([0.0, 0.0, 1.0]), [0.0, 0.0, 1.0]
+    for u1, u2 in rng.random((200, 2)):
+        ok1, w1 = B.bsdf_sample([1, 1, 1, 1, alpha], n, wi, u1, u2)
+        ok2, w2 = B.bsdf_sample([2, 1, 1, 1, alpha], n, wi, u1, u2)
+        assert ok1 == ok2
+        if ok1:
+            assert np.allclose(w1, w2, atol=1e-9), (w1, w2)
+            assert B.bsdf([2, 1, 1, 1, alpha], n, wi, w2)[1] == pytest.approx(B.bsdf([1, 1, 1, 1, alpha], n, wi, w1)[1],
+                                                                              rel=1e-9)
+
+
+@pytest.mark.parametrize("alpha", [0.1, 0.4, 0.9])
+def test_vndf_sample_weight_is_g1_of_wo(alpha):
+    """With F0 = 1 (Fresnel 1) every visible-normal sample has weight f cos_o / pdf = G1(wo) exactly
+    (f = D G1(wi) G1(wo) / (4 cos_i cos_o), pdf = G1(wi) D / (4 cos_i)), at any incidence."""
+    rng = np.random.default_rng(5)
+    n = np.array([0.0, 0.0, 1.0])
+    mat = [2, 1.0, 1.0, 1.0, alpha]
+    for th in (0.2, 0.9, 1.4):
+        wi = [math.sin(th), 0.0, math.cos(th)]
+        for u1, u2 in rng.random((300, 2)):
+            ok, wo = B.bsdf_sample(mat, n, wi, u1, u2)
+            if not ok:
+                continue
+            ev, pdf = B.bsdf(mat, n, wi, wo)
+            assert ev[0] * wo[2] / pdf == pytest.approx(_g1(alpha, wo[2]), rel=1e-9)
+
+
+def test_vndf_pdf_is_not_symmetric_but_eval_is():
+    """pdf(wo | wi) conditions on wi: G1(wi) / cos_i differs from G1(wo) / cos_o, unlike the classic
+    half-vector pdf; f stays reciprocal."""
+    n = np.array([0.0, 0.0, 1.0])
+    wi, wo = [math.sin(1.2), 0.0, math.cos(1.2)], [-math.sin(0.3), 0.0, math.cos(0.3)]
+    ea, pa = B.bsdf([2, 1, 1, 1, 0.5], n, wi, wo)
+    eb, pb = B.bsdf([2, 1, 1, 1, 0.5], n, wo, wi)
+    assert ea[0] == pytest.approx(eb[0], rel=1e-12)
+    assert pa / pb == pytest.approx((_g1(0.5, wi[2]) / wi[2]) / (_g1(0.5, wo[2]) / wo[2]), rel=1e-9)
+    _, qa = B.bsdf([1, 1, 1, 1, 0.5], n, wi, wo)
+    _, qb = B.bsdf([1, 1, 1, 1, 0.5], n, wo, wi)
+    assert qa == pytest.approx(qb, rel=1e-12)
 
 
 def test_lambert_histogram_chi_square():
