@@ -97,7 +97,10 @@ enum {
   RR_RECONNECT = 2u,   /* "keep vertex the same" reconnection; requires RR_TWO_WAY */
   RR_REJECT_MULTI = 4u,/* reject diverged pairs with >= 2 dynamic vertices; requires RR_TWO_WAY */
   RR_ACCUMULATE = 8u,  /* add into d_image instead of overwriting it */
-  RR_COUNT_TRAVERSAL = 16u /* count BVH node fetches / triangle tests into rr_stats (diagnostic, ~3% slower) */
+  RR_COUNT_TRAVERSAL = 16u,/* count BVH node fetches / triangle tests into rr_stats (diagnostic, ~3% slower) */
+  RR_VNDF = 32u            /* sample GGX directions from the visible normals of the incoming direction (Heitz
+                              2018) instead of D(h)|n.h|; pdfs and MIS follow.  A variance-only variant
+                              (SURVEY 8(f) row 4); residual renders only (the primal renderer ignores it) */
 };
 #define RR_PAPER_FLAGS (RR_TWO_WAY | RR_RECONNECT | RR_REJECT_MULTI)
 #define RR_MAX_DEPTH 10

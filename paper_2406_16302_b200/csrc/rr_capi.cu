@@ -38,7 +38,7 @@ struct rr_ctx {
   std::vector<float> inst_bbox;   // 6 per instance, object space
   // device buffers
   DevBuf<float4> nodes, ltris, lxf, tverts, mat, obj_emit;
-  DevBuf<uint32_t> d_tri_obj, obj_flags, mat_type, obj_mat0, obj_mat1, emit_tris, edited_tris, moved_tris;
+  DevBuf<uint32_t> d_tri_obj, obj_flags, mat_type, mat_type_vndf, obj_mat0, obj_mat1, emit_tris, edited_tris, moved_tris;
   DevBuf<int> d_obj_inst, obj_emitter, emit_off, emit_cnt;
   DevBuf<float> emit_pL, emit_cdf, edited_cdf, moved_cdf;
   DevBuf<unsigned long long> stats, work;
@@ -644,6 +644,8 @@ rr_status rr_set_edit(rr_ctx* c, uint32_t n, const rr_edit* edits) {
     }
     c->mat.upload(m4.data(), m4.size());
     c->mat_type.upload(mt.data(), mt.size());
+    for (auto& t : mt) t = t == RR_GGX ? 2u : t;  // RR_VNDF renders: GGX sampled from the visible normals
+    c->mat_type_vndf.upload(mt.data(), mt.size());
     c->obj_mat0.upload(om0.data(), O);
     c->obj_mat1.upload(om1.data(), O);
     c->obj_flags.upload(flags.data(), O);
@@ -680,6 +682,8 @@ static rr_status check_args(rr_ctx* c, const rr_render_args* a) {
   if (a->layer_mask & ~0x7Fu) return fail(c, RR_E_INVALID, "unknown layer bits");
   if (!(a->flags & RR_TWO_WAY) && (a->flags & (RR_RECONNECT | RR_REJECT_MULTI)))
     return fail(c, RR_E_INVALID, "RR_RECONNECT / RR_REJECT_MULTI require RR_TWO_WAY");
+  if (a->flags & ~(RR_TWO_WAY | RR_RECONNECT | RR_REJECT_MULTI | RR_ACCUMULATE | RR_COUNT_TRAVERSAL | RR_VNDF))
+    return fail(c, RR_E_INVALID, "unknown flag bits");
   if (a->shard_count == 0 || a->shard_index >= a->shard_count) return fail(c, RR_E_INVALID, "bad shard");
   return RR_OK;
 }
@@ -705,6 +709,7 @@ static KArgs make_kargs(rr_ctx* c, const rr_render_args* a, uint32_t mask, int l
   K.mask = mask;
   K.two_way = (a->flags & RR_TWO_WAY) ? 1 : 0;
   K.count = (a->flags & RR_COUNT_TRAVERSAL) ? 1 : 0;
+  K.mat_type_vndf = (a->flags & RR_VNDF) ? c->mat_type_vndf.p : nullptr;
   K.reconnect = (a->flags & RR_RECONNECT) ? 1 : 0;
   K.reject_multi = (a->flags & RR_REJECT_MULTI) ? 1 : 0;
   K.seed = a->seed;

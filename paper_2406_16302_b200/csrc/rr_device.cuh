@@ -133,7 +133,7 @@ struct DevScene {
   const int* obj_inst;
   const uint32_t* obj_mat[2];
   const float4* mat;         // albedo rgb, alpha
-  const uint32_t* mat_type;
+  const uint32_t* mat_type;   // 0 Lambert, 1 GGX; RR_VNDF renders get a copy with GGX as 2 (visible normals)
   const float4* obj_emit;
   const int* obj_emitter;
   int n_emit;
@@ -212,14 +212,45 @@ __device__ __forceinline__ float3 bsdf_eval(const Mat& m, float3 n, float3 wi, f
   float3 F = m.albedo + (f3(1.f, 1.f, 1.f) - m.albedo) * fw;
   return F * (D * G / (4.0f * ci * co));
 }
+// GGX visible-normal sampling (RR_VNDF) is compiled only into the kernels of rr_residual_vndf.cu
+// (RR_VNDF_KERNELS = 1): its branches in the default kernels cost 2.5% of a config-4 render
+#if defined(RR_VNDF_KERNELS) && RR_VNDF_KERNELS
+__device__ __forceinline__ float ggx_vndf_pdf(float a, float ci, float3 ns, float3 h) {
+  return ggx_G1(a, ci) * ggx_D(a, ns, h) / (4.0f * ci);
+}
+#endif
 __device__ __forceinline__ float bsdf_pdf(const Mat& m, float3 n, float3 wi, float3 wo) {
   float3 ns = dot3(n, wi) > 0.0f ? n : n * -1.0f;
   float ci = dot3(ns, wi), co = dot3(ns, wo);
   if (!(ci > 0.0f) || !(co > 0.0f)) return 0.0f;
   if (m.type == 0) return co * RR_INV_PI_F;
   float3 h = norm3_exact(wi + wo);
+  // VNDF: D_wi(h) / (4 wo.h) with D_wi(h) = G1(wi) (wi.h) D(h) / (n.wi) and wo.h = wi.h
+#if defined(RR_VNDF_KERNELS) && RR_VNDF_KERNELS
+  if (m.type == 2) return ggx_vndf_pdf(m.alpha, ci, ns, h);
+#endif
   return ggx_D(m.alpha, ns, h) * fabsf(dot3(ns, h)) / (4.0f * fabsf(dot3(wo, h)));
 }
+// half vector from the GGX visible normals of wi (Heitz 2018, isotropic): stretch wi, sample the projected
+// hemisphere of the stretched view (disk point warped by s = (1 + Vh_z) / 2), unstretch; frame of to_world
+#if defined(RR_VNDF_KERNELS) && RR_VNDF_KERNELS
+__device__ __forceinline__ float3 ggx_vndf_half(float a, float3 ns, float3 wi, float u1, float u2) {
+  float3 b1, b2;
+  onb(ns, b1, b2);
+  float3 vh = norm3_exact(f3(a * dot3(wi, b1), a * dot3(wi, b2), dot3(wi, ns)));
+  float lensq = vh.x * vh.x + vh.y * vh.y;
+  float3 T1 = lensq > 0.0f ? f3(-vh.y, vh.x, 0.0f) * (1.0f / sqrtf(lensq)) : f3(1.0f, 0.0f, 0.0f);
+  float3 T2 = cross3(vh, T1);
+  float r = sqrtf(u1), sp, cp;
+  sincosf(2.0f * RR_PI_F * u2, &sp, &cp);
+  float t1 = r * cp, t2 = r * sp;
+  float sw = 0.5f * (1.0f + vh.z);
+  t2 = (1.0f - sw) * sqrtf(1.0f - t1 * t1) + sw * t2;
+  float3 nh = T1 * t1 + T2 * t2 + vh * sqrtf(fmaxf(0.0f, 1.0f - t1 * t1 - t2 * t2));
+  float3 hl = norm3_exact(f3(a * nh.x, a * nh.y, fmaxf(0.0f, nh.z)));
+  return to_world(ns, hl.x, hl.y, hl.z);
+}
+#endif
 __device__ __forceinline__ bool bsdf_sample(const Mat& m, float3 n, float3 wi, float u1, float u2, float3& wo) {
   float3 ns = dot3(n, wi) > 0.0f ? n : n * -1.0f;
   if (m.type == 0) {
@@ -230,6 +261,15 @@ __device__ __forceinline__ bool bsdf_sample(const Mat& m, float3 n, float3 wi, f
     return true;
   }
   float a = m.alpha;
+#if defined(RR_VNDF_KERNELS) && RR_VNDF_KERNELS
+  if (m.type == 2) {
+    float3 h = norm3_exact(ggx_vndf_half(a, ns, wi, u1, u2));
+    float3 w = h * (2.0f * dot3(wi, h)) - wi;
+    if (!(dot3(w, ns) > 0.0f)) return false;
+    wo = norm3_exact(w);
+    return true;
+  }
+#endif
   float tan2 = a * a * u1 / (1.0f - u1);
   float ct = 1.0f / sqrtf(1.0f + tan2);
   float st = sqrtf(tan2) * ct;  // sin = tan cos: no cancellation for the small angles of sharp lobes

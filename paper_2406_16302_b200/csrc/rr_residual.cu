@@ -14,6 +14,9 @@
 // The two walks of a single-walk sample run in lockstep so that the static-BLAS traversal is shared while
 // they have not diverged (A3), the reconnection ("keep vertex the same") is decided at the first
 // diverged rough vertex, and connections are evaluated and splatted as soon as they are formed.
+#ifndef RR_VNDF_KERNELS
+#define RR_VNDF_KERNELS 0  // 1: this TU is the RR_VNDF instantiation (rr_residual_vndf.cu)
+#endif
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -24,6 +27,13 @@
 #include "rr_shade.cuh"
 
 namespace rr {
+// the state machines and kernels live in a namespace per instantiation: kplain (default) and kvndf (GGX
+// visible-normal sampling compiled in), so that the default kernels carry no code of the variant
+#if RR_VNDF_KERNELS
+namespace kvndf {
+#else
+namespace kplain {
+#endif
 
 #define NQ 10
 #define FULLMASK 0xffffffffu
@@ -148,7 +158,7 @@ __device__ void start_consume(const DevScene& S, int tech, int F, const SStart& 
 }
 
 // issue the queries of walk vertex m (connection at m, walk step from m, pending reconnection/suffix checks)
-__device__ void single_issue(const DevScene& S, const KArgs& A, SState& st, Batch& B) {
+__device__ __forceinline__ void single_issue(const DevScene& S, const KArgs& A, SState& st, Batch& B) {
   const int F = A.side, Fb = 1 - F, l = A.tech, lq = A.tech_q, D = A.max_depth, m = st.m;
   const bool Lroot = (l == 1 || l == 4);
   const int maxW = D - 1 > 1 ? D - 1 : 1;
@@ -229,7 +239,7 @@ __device__ void single_issue(const DevScene& S, const KArgs& A, SState& st, Batc
 }
 
 // consume the results of walk vertex m; returns false when the sample is finished
-__device__ bool single_consume(const DevScene& S, const KArgs& A, SState& st, const Batch& B, Out& o) {
+__device__ __forceinline__ bool single_consume(const DevScene& S, const KArgs& A, SState& st, const Batch& B, Out& o) {
   const int F = A.side, Fb = 1 - F, l = A.tech, D = A.max_depth, m = st.m;
   const bool Lroot = (l == 1 || l == 4);
   const int maxW = D - 1 > 1 ? D - 1 : 1;
@@ -420,7 +430,7 @@ __device__ bool single_consume(const DevScene& S, const KArgs& A, SState& st, co
 }
 
 // advance one single-walk sample: consume the last batch (if any), issue the next; false when done
-__device__ bool single_step(const DevScene& S, const KArgs& A, SState& st, Batch& B, Out& o) {
+__device__ __forceinline__ bool single_step(const DevScene& S, const KArgs& A, SState& st, Batch& B, Out& o) {
   const int F = A.side, Fb = 1 - F;
   while (true) {
     if (st.pc == 0) {
@@ -890,6 +900,27 @@ __global__ void __launch_bounds__(RR_BLOCK, RR_MIN_BLOCKS) k_residual_bidir(cons
   residual_loop<BState, true, COUNT>(S, A);
 }
 
+inline void launch_kernels(const DevScene& S, const KArgs& A, int grid, cudaStream_t st) {
+  const bool bidir = A.tech == 3 || A.tech == 6;
+  if (A.count) {
+    if (bidir) k_residual_bidir<true><<<grid, RR_BLOCK, 0, st>>>(S, A);
+    else k_residual_single<true><<<grid, RR_BLOCK, 0, st>>>(S, A);
+  } else {
+    if (bidir) k_residual_bidir<false><<<grid, RR_BLOCK, 0, st>>>(S, A);
+    else k_residual_single<false><<<grid, RR_BLOCK, 0, st>>>(S, A);
+  }
+}
+}  // namespace kplain / kvndf
+
+#if RR_VNDF_KERNELS
+void launch_residual_vndf(const DevScene& S0, const KArgs& A, int grid, cudaStream_t st) {
+  DevScene S = S0;
+  S.mat_type = A.mat_type_vndf;  // GGX = 2: visible-normal sampling
+  kvndf::launch_kernels(S, A, grid, st);
+}
+#else
+using namespace kplain;  // helpers of the state machines (bit(), ...) used by the test kernels below
+
 __global__ void k_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out) {
   uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
@@ -952,8 +983,8 @@ int residual_grid(bool bidir, uint64_t n) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_residual_single<false>, RR_BLOCK, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_residual_bidir<false>, RR_BLOCK, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], kplain::k_residual_single<false>, RR_BLOCK, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], kplain::k_residual_bidir<false>, RR_BLOCK, 0);
   }
   uint64_t g = (n + RR_BLOCK - 1) / RR_BLOCK;
   uint64_t cap = (uint64_t)sms * (uint64_t)std::max(1, occ[bidir ? 1 : 0]);
@@ -961,14 +992,8 @@ int residual_grid(bool bidir, uint64_t n) {
 }
 int residual_block() { return RR_BLOCK; }
 void launch_residual(const DevScene& S, const KArgs& A, int grid, cudaStream_t st) {
-  const bool bidir = A.tech == 3 || A.tech == 6;
-  if (A.count) {
-    if (bidir) k_residual_bidir<true><<<grid, RR_BLOCK, 0, st>>>(S, A);
-    else k_residual_single<true><<<grid, RR_BLOCK, 0, st>>>(S, A);
-  } else {
-    if (bidir) k_residual_bidir<false><<<grid, RR_BLOCK, 0, st>>>(S, A);
-    else k_residual_single<false><<<grid, RR_BLOCK, 0, st>>>(S, A);
-  }
+  if (A.mat_type_vndf) launch_residual_vndf(S, A, grid, st);  // RR_VNDF: the other instantiation
+  else kplain::launch_kernels(S, A, grid, st);
 }
 void launch_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out, cudaStream_t st) {
   k_philox<<<(n + 255) / 256, 256, 0, st>>>(n, ctr, k0, k1, out);
@@ -980,4 +1005,5 @@ void launch_segment(const DevScene& S, uint32_t n, const float* segs, float* out
   k_segment<<<(n + 127) / 128, 128, 0, st>>>(S, n, segs, out);
 }
 
+#endif  // RR_VNDF_KERNELS
 }  // namespace rr

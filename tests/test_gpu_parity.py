@@ -247,6 +247,15 @@ def test_records_config2_material_edit(torch_cuda):
     record_parity(w, w.args, n_per=40000)
 
 
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_records_vndf(torch_cuda, cfg):
+    """GGX visible-normal sampling (RR_VNDF): config 2's GGX cube (alpha 0.5 -> 0.1) and
+    config 3's GGX objects at full size, sampled like the paper-mode tests."""
+    w = S.config2() if cfg == 2 else S.load_config(3)
+    args = dataclasses.replace(w.args, flags=w.args.flags | S.VNDF)
+    record_parity(w, args, n_per=40000 if cfg == 2 else 3000)
+
+
 def test_records_occluder_reveal(torch_cuda):
     w = S.occluder_reveal(32, 32, spp=8, max_depth=5)
     record_parity(w, w.args)
@@ -320,7 +329,7 @@ def test_identity_edit_exact_zero_gpu(torch_cuda):
     torch = torch_cuda
     w = S.cornell_identity(64, 64, spp=8, max_depth=6)
     r = _renderer(w)
-    for flags in (S.PAPER_FLAGS, S.TWO_WAY, 0):
+    for flags in (S.PAPER_FLAGS, S.TWO_WAY, 0, S.PAPER_FLAGS | S.VNDF):
         img = r.render_residual(dataclasses.replace(w.args, flags=flags))
         torch.cuda.synchronize()
         assert int(torch.count_nonzero(img)) == 0
@@ -366,7 +375,7 @@ def test_invalid_arguments_are_refused(torch_cuda):
     w = S.config1(16, 16)
     r = _renderer(w)
     for bad in (dict(technique_mask=0x3F), dict(spp=3), dict(max_depth=0), dict(max_depth=11),
-                dict(flags=S.RECONNECT), dict(layer_mask=0x80)):
+                dict(flags=S.RECONNECT), dict(layer_mask=0x80), dict(flags=S.PAPER_FLAGS | 64)):
         with pytest.raises(RRError):
             r.render_residual(dataclasses.replace(w.args, **bad))
     for bad in (dict(state=2), dict(spp=0), dict(max_depth=0), dict(max_depth=11)):
