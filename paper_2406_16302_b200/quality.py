@@ -7,7 +7,8 @@ Estimators of the residual Delta = I(new) - I(old) compared against a high-sampl
   * "residual"        -- the paper's method: all seven techniques, path mapping, two-way (P:L285-436);
 ablations of the method (the mapping components of P:L387-436, one at a time):
   * "residual_replay" -- two-way, no reconnection: diverged paths are replayed only (RR_RECONNECT off);
-  * "residual_one_way"-- one side per technique, replay only (flags 0; SPEC's "mapping off" run knob).
+  * "residual_one_way"-- one side per technique, replay only (flags 0; SPEC's "mapping off" run knob);
+and the paper's mode with GGX visible-normal sampling ("residual_vndf", RR_VNDF).
 Each is timed with CUDA events on the device; mse() and ssim() are taken against the reference and
 efficiency = 1 / (mse * seconds).  Scenes are the synthetic stand-ins of rr_inputs (no
 measured data).
@@ -57,6 +58,8 @@ def estimators(r, args, spp: int, seed: int = 0, ablations: bool = False) -> Dic
         out["residual_replay"] = _timed(lambda: r.render_residual(rep).clone())
         one = dataclasses.replace(args, spp=spp, seed=seed + 16, flags=0)
         out["residual_one_way"] = _timed(lambda: r.render_residual(one).clone())
+        vn = dataclasses.replace(full, seed=seed + 17, flags=PAPER_FLAGS | 32)
+        out["residual_vndf"] = _timed(lambda: r.render_residual(vn).clone())
     return out
 
 
