@@ -63,3 +63,13 @@ def test_pfm_roundtrip(tmp_path):
     rgba = rng.normal(size=(3, 2, 4)).astype(np.float32)
     write_pfm(p, rgba)
     assert np.array_equal(read_pfm(p), rgba[..., :3])
+
+
+def test_missing_extension_fails_loudly(tmp_path):
+    """No CPU fallback: without the CUDA library the product path raises (in a fresh interpreter)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, RR_LIB_VARIANT=str(tmp_path / "absent.so"))
+    r = subprocess.run([sys.executable, "-c", "from paper_2406_16302_b200 import native; native.lib()"],
+                       cwd=ROOT, env=env, capture_output=True, text=True)
+    assert r.returncode != 0 and "CUDA extension missing" in r.stderr, r.stderr[-500:]
