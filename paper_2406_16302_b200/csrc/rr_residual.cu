@@ -791,7 +791,9 @@ __device__ __forceinline__ uint64_t fetch_work(unsigned long long* counter, bool
 // advance their samples in lockstep, then trace the queries the step issued through the single traversal
 // site (rr_query.cuh).
 // ------------------------------------------------------------------------------------------------
-#define RR_BLOCK 128
+#ifndef RR_BLOCK
+#define RR_BLOCK 128  // threads per block of the residual kernels
+#endif
 #ifndef RR_MIN_BLOCKS
 #define RR_MIN_BLOCKS 16  // resident blocks per SM requested from the register allocator (32 registers:
                           // latency hiding beats the spills)
