@@ -247,12 +247,12 @@ def test_records_config2_material_edit(torch_cuda):
     record_parity(w, w.args, n_per=40000)
 
 
-@pytest.mark.parametrize("cfg", [2, 3])
-def test_records_vndf(torch_cuda, cfg):
-    """GGX visible-normal sampling (RR_VNDF): config 2's GGX cube (alpha 0.5 -> 0.1) and
-    config 3's GGX objects at full size, sampled like the paper-mode tests."""
+@pytest.mark.parametrize("cfg,flags", [(2, S.PAPER_FLAGS), (2, 0), (3, S.PAPER_FLAGS)])
+def test_records_vndf(torch_cuda, cfg, flags):
+    """GGX visible-normal sampling (RR_VNDF): config 2's GGX cube (alpha 0.5 -> 0.1; paper
+    mode and one-way replay) and config 3's GGX objects at full size, sampled like the paper-mode tests."""
     w = S.config2() if cfg == 2 else S.load_config(3)
-    args = dataclasses.replace(w.args, flags=w.args.flags | S.VNDF)
+    args = dataclasses.replace(w.args, flags=flags | S.VNDF)
     record_parity(w, args, n_per=40000 if cfg == 2 else 3000)
 
 
