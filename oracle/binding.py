@@ -86,6 +86,8 @@ def lib():
         L.orc_residual.argtypes = [P, C.POINTER(Args), C.c_int, C.c_int, C.c_uint64, C.c_uint64, D,
                                    C.POINTER(Record), C.c_int64, C.POINTER(C.c_int64), C.POINTER(Stats)]
         L.orc_primal.argtypes = [P, C.c_int, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, D, C.POINTER(Stats)]
+        L.orc_primal_streams.argtypes = [P, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, D,
+                                         C.POINTER(Stats)]
         L.orc_philox.argtypes = [C.POINTER(C.c_uint32)] * 3
         L.orc_u01.restype = C.c_double
         L.orc_u01.argtypes = [C.c_uint32]
@@ -114,6 +116,11 @@ def lib():
         L.orc_set_area.argtypes = [P, C.c_int]
         L.orc_project.argtypes = [P, D]
         L.orc_debug_sample.argtypes = [P, C.POINTER(Args), C.c_int, C.c_int, C.c_uint64]
+        L.orc_t3_light_dir.argtypes = [D, C.c_double, C.c_double, D]
+        L.orc_reconnections.restype = C.c_int64
+        L.orc_reconnections.argtypes = [P, C.POINTER(Args), C.c_int, C.c_int, C.c_uint64, C.c_uint64, D, C.c_int64]
+        L.orc_pdf_check.restype = C.c_int64
+        L.orc_pdf_check.argtypes = [P, C.POINTER(Args), C.c_int, C.c_int, C.c_uint64, C.c_uint64, D, C.c_int64]
     return _lib
 
 
@@ -236,6 +243,12 @@ class Oracle:
         """Samples per (technique, side): N_pix spp / 2 two-way, N_pix spp one-way."""
         return self.npix * args.spp // 2 if (args.flags & 1) else self.npix * args.spp
 
+    @staticmethod
+    def sides(args):
+        """Sides that run: both two-way; side N only one-way (the paired technique's replayed paths in O are
+        counted from it) and in the diagnostic one-way ablation."""
+        return (0, 1) if (args.flags & 1) else (0,)
+
     def render_residual(self, args, records: bool = False, techniques=None, limit: Optional[int] = None):
         """Full residual image (H,W,3) over every enabled technique and side."""
         mask = self.effective_mask(args.technique_mask)
@@ -244,7 +257,7 @@ class Oracle:
         n = self.sample_range(args)
         if limit is not None:
             n = min(n, limit)
-        sides = (0, 1) if (args.flags & 1) else (0,)
+        sides = self.sides(args)
         for l in range(1, 8):
             if not (mask >> (l - 1)) & 1:
                 continue
@@ -263,6 +276,34 @@ class Oracle:
         i1 = self.npix * spp if i1 is None else i1
         lib().orc_primal(self.h, F, seed, max_depth, i0, i1, dptr(img), C.byref(st))
         return img / spp, st.as_dict()
+
+    def pdf_check(self, args, tech: int, side: int, i0: int, i1: int) -> np.ndarray:
+        """[n, 3]: per connection (generator-recorded density, eval_path pdf of the producing candidate or -1,
+        number of candidates) -- the C5 self-consistency pin."""
+        a = self.make_args(args)
+        cap = 64 * (i1 - i0) + 64
+        out = np.zeros(3 * cap)
+        n = lib().orc_pdf_check(self.h, C.byref(a), tech, side, i0, i1, dptr(out), cap)
+        return out[:3 * min(n, cap)].reshape(-1, 3)
+
+    def reconnections(self, args, tech: int, side: int, i0: int, i1: int) -> np.ndarray:
+        """[n, 39]: accepted reconnections {j - w, R, R of the inverse map, (p, n) of v_{w-1}, v_w, v'_{w-1},
+        v'_w, v_{w+1}, v_{w+2}} (the R pins of SURVEY 8(c) C11)."""
+        a = self.make_args(args)
+        cap = 16 * (i1 - i0) + 16
+        out = np.zeros(39 * cap)
+        n = lib().orc_reconnections(self.h, C.byref(a), tech, side, i0, i1, dptr(out), cap)
+        return out[:39 * min(n, cap)].reshape(-1, 39)
+
+    def primal_difference(self, seed: int, spp: int, max_depth: int) -> np.ndarray:
+        """I^D(N) - I^D(O) from the primal renderer with the SAME random numbers in both states (correlated,
+        unbiased; independent of the residual estimator's code)."""
+        out = []
+        for F in (0, 1):
+            img = np.zeros((self.H, self.W, 3), np.float64)
+            lib().orc_primal_streams(self.h, F, 0, seed, max_depth, 0, self.npix * spp, dptr(img), None)
+            out.append(img / spp)
+        return out[0] - out[1]
 
     def debug_sample(self, args, tech, side, i):
         a = self.make_args(args)
@@ -329,6 +370,13 @@ def bsdf_sample(mat, n, wi, u1, u2):
     wo = np.zeros(3)
     ok = lib().orc_bsdf_sample(dptr(vec(mat)), dptr(vec(n)), dptr(vec(wi)), u1, u2, dptr(wo))
     return bool(ok), wo
+
+
+def t3_light_dir(n, u3, u4):
+    """T3's cosine-weighted emitter-side start direction at a dynamic point with normal n; (w, pdf)."""
+    out = np.zeros(4)
+    lib().orc_t3_light_dir(dptr(vec(n)), u3, u4, dptr(out))
+    return out[:3], out[3]
 
 
 def geometric_term(x, nx, y, ny):

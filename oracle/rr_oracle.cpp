@@ -566,12 +566,14 @@ Vtx sample_set(const Scene& S, const Scene::TriSet& ts, int F, double u0, double
   v.kind = K_SURF;
   return v;
 }
-// NEE emitter sample: object o = min(floor(d3 n_obj), n_obj-1), area-uniform within it (C3)
-Vtx sample_emitter(const Scene& S, const double d[8]) {
+// NEE emitter sample: object o = min(floor(d3 n_obj), n_obj-1), area-uniform within it (C3).
+// *pdf (optional): the density the sampler drew x_L with, 1/n_obj * 1/A_o, from its own choice of o.
+Vtx sample_emitter(const Scene& S, const double d[8], double* pdf = nullptr) {
   int ne = (int)S.emitters.size();
   int e = std::min((int)std::floor(d[3] * ne), ne - 1);
   Vtx v = sample_set(S, S.emitters[e], 0, d[4], d[5], d[6]);  // emitters never move
   v.kind = K_LIGHT;
+  if (pdf) *pdf = (1.0 / ne) * (1.0 / S.emitters[e].area);
   return v;
 }
 double p_light(const Scene& S, const Vtx& L) {
@@ -592,6 +594,12 @@ struct Path {
   int pixel = -1;
 };
 
+struct Cand {
+  int tech;
+  int elem;  // vertex index or edge index
+  int sub;   // crossing index on the edge
+};
+
 struct Eval {
   V3 f = v3(0, 0, 0);
   double Pi = 0;
@@ -599,6 +607,8 @@ struct Eval {
   bool walk_edge_blocked = false;
   std::vector<int> edge_vis;
   std::vector<std::vector<Crossing>> cross;
+  std::vector<Cand> cands;      // the candidates of Pi, in order, and each one's technique pdf (C5 table)
+  std::vector<double> cand_p;
 };
 
 double geo(const Vtx& a, const Vtx& b) {  // G = |cos_a||cos_b| / d^2 (n_{x_E} := camera forward)
@@ -626,12 +636,6 @@ double p_cam(const Scene& S, const Vtx& x1) {
   if (!(c > 0)) return 0.0;
   return std::fabs(dot(x1.n, w)) / (S.Aplane * c * c * c * d2);
 }
-
-struct Cand {
-  int tech;
-  int elem;  // vertex index or edge index
-  int sub;   // crossing index on the edge
-};
 
 // Candidate techniques of a path with k vertices:
 // T7 always; one per dynamic vertex x_i (i = k-2 -> T1, i = 1 -> T2, else T3); one per ghost
@@ -664,6 +668,7 @@ struct Ctx {
   const Scene* S;
   int mask;     // effective technique mask
   Counters C;
+  std::vector<double>* recon_out = nullptr;  // test export: geometry of accepted reconnections (orc_reconnections)
 };
 
 Eval eval_path(Ctx& cx, int F, const Path& P, bool check_walk_vis = true) {
@@ -776,7 +781,9 @@ Eval eval_path(Ctx& cx, int F, const Path& P, bool check_walk_vis = true) {
       }
     }
     Pi += p;
+    ev.cand_p.push_back(p);
   }
+  ev.cands = cands;
   ev.Pi = Pi;
   return ev;
 }
@@ -788,6 +795,10 @@ struct Walk {
   std::vector<Vtx> v;   // v[0] = predecessor of the first walk vertex (E, x_L, x_D, ...); v[1..] walk
   std::vector<V3> wo;   // wo[m]: direction sampled at v[m] (valid if wo_ok[m])
   std::vector<int> wo_ok;
+  // pA[m] (m >= 1): the area density with which the generator produced v[m], recorded at generation time
+  // from the sampled direction and hit distance (pdf_w |n.w| / t^2, or the technique's start density).
+  // Only the technique-pdf self-consistency pin reads it.
+  std::vector<double> pA;
   int n() const { return (int)v.size() - 1; }
 };
 
@@ -801,6 +812,7 @@ struct Gen {
   Walk A;               // single walk; sensor-side walk for T3/T6
   Walk B;               // emitter-side walk for T3/T6
   bool emit_direct = false;  // T7: x_1 reached (k = 2 candidate)
+  double pdf0 = 1.0;    // recorded density of the start event not held in A.pA / B.pA (x_L; T3 x_D; T6 (x_G, d))
 };
 
 // continue a walk from v[n] using slots slot0 + m for walk vertex m, until `nmax` walk vertices
@@ -823,7 +835,17 @@ void extend_walk(Ctx& cx, int F, const Stream& st, Walk& w, int slot0, int nmax)
     Hit h = closest(S, F, cur.p, wo, cur.tri, &cx.C);
     if (!h.ok) break;
     w.v.push_back(vtx_of_hit(cur.p, wo, h));
+    w.pA.resize(w.v.size(), 0.0);
+    w.pA[m + 1] = bsdf_pdf(mt, cur.n, wi, wo) * std::fabs(dot(h.tri->n, wo)) / (h.t * h.t);
   }
+}
+
+// T3's emitter-side direction at x_D: cosine-weighted about +n as wound (C12 #8); *pdf = the
+// density of the sampled local z = sqrt(1 - u3), i.e. cos(theta) / pi
+V3 t3_light_dir(V3 n, double u3, double u4, double* pdf) {
+  double r = std::sqrt(u3), phi = 2.0 * PI * u4, z = std::sqrt(std::max(0.0, 1.0 - u3));
+  *pdf = z / PI;
+  return normalize(local_to_world(n, r * std::cos(phi), r * std::sin(phi), z));
 }
 
 Gen generate(Ctx& cx, int tech, int F, const Stream& st, int D) {
@@ -846,6 +868,10 @@ Gen generate(Ctx& cx, int tech, int F, const Stream& st, int D) {
       g.ok = true;
       g.A.v.push_back(E);
       g.A.v.push_back(vtx_of_hit(S.cam_pos, dir, h));
+      {  // film point uniform over the film plane (density 1/A_plane) -> solid angle (/cos^3) -> area
+        double c = dot(dir, S.cf);
+        g.A.pA = {0.0, (1.0 / S.Aplane) / (c * c * c) * std::fabs(dot(h.tri->n, dir)) / (h.t * h.t)};
+      }
       g.emit_direct = true;
       extend_walk(cx, F, st, g.A, 0, D - 1);
       return g;
@@ -853,7 +879,7 @@ Gen generate(Ctx& cx, int tech, int F, const Stream& st, int D) {
     case 1: {  // dynamic from emitter
       if (S.edited_set.tris.empty()) return g;
       Vtx xd = sample_set(S, S.edited_set, F, d0[0], d0[1], d0[2]);
-      Vtx xl = sample_emitter(S, d0);
+      Vtx xl = sample_emitter(S, d0, &g.pdf0);
       if (!(dot(xl.n, xd.p - xl.p) > 0)) return g;          // back-facing emitter
       if (!visible(S, F, xd.p, xl.p, xd.tri, xl.tri, &cx.C)) return g;  // "fails if blocked" P:L286
       g.ok = true;
@@ -861,6 +887,7 @@ Gen generate(Ctx& cx, int tech, int F, const Stream& st, int D) {
       g.xL = xl;
       g.A.v.push_back(xl);
       g.A.v.push_back(xd);
+      g.A.pA = {0.0, 1.0 / S.edited_set.area};
       extend_walk(cx, F, st, g.A, 0, D - 1);
       return g;
     }
@@ -875,14 +902,15 @@ Gen generate(Ctx& cx, int tech, int F, const Stream& st, int D) {
       g.start = xd;
       g.A.v.push_back(E);
       g.A.v.push_back(xd);
+      g.A.pA = {0.0, 1.0 / S.edited_set.area};
       extend_walk(cx, F, st, g.A, 0, D - 1);
       return g;
     }
     case 3: {  // dynamic two ends
       if (S.edited_set.tris.empty()) return g;
       Vtx xd = sample_set(S, S.edited_set, F, d0[0], d0[1], d0[2]);
-      double r = std::sqrt(d0[3]), phi = 2.0 * PI * d0[4];
-      V3 wl = normalize(local_to_world(xd.n, r * std::cos(phi), r * std::sin(phi), std::sqrt(std::max(0.0, 1.0 - d0[3]))));
+      double pdf_wl;
+      V3 wl = t3_light_dir(xd.n, d0[3], d0[4], &pdf_wl);
       Mat mt = mat_of(S, xd.obj, F);
       V3 we;
       if (!bsdf_sample(mt, xd.n, wl, d0[6], d0[7], we)) return g;
@@ -893,10 +921,14 @@ Gen generate(Ctx& cx, int tech, int F, const Stream& st, int D) {
       if (!hz.ok) return g;
       g.ok = true;
       g.start = xd;
+      g.pdf0 = 1.0 / S.edited_set.area;
       g.B.v.push_back(xd);
       g.B.v.push_back(vtx_of_hit(xd.p, wl, hy));
+      // cosine density of omega_L, and the BSDF density of omega_E
+      g.B.pA = {0.0, pdf_wl * std::fabs(dot(hy.tri->n, wl)) / (hy.t * hy.t)};
       g.A.v.push_back(xd);
       g.A.v.push_back(vtx_of_hit(xd.p, we, hz));
+      g.A.pA = {0.0, bsdf_pdf(mt, xd.n, wl, we) * std::fabs(dot(hz.tri->n, we)) / (hz.t * hz.t)};
       extend_walk(cx, F, st, g.B, 16, D - 3);
       extend_walk(cx, F, st, g.A, 0, D - 3);
       return g;
@@ -904,7 +936,7 @@ Gen generate(Ctx& cx, int tech, int F, const Stream& st, int D) {
     case 4: {  // ghost from emitter
       if (S.moved_set.tris.empty()) return g;
       Vtx xg = sample_set(S, S.moved_set, 1 - F, d0[0], d0[1], d0[2]);  // ghost_F = moved at M_Fbar
-      Vtx xl = sample_emitter(S, d0);
+      Vtx xl = sample_emitter(S, d0, &g.pdf0);
       V3 dv = xg.p - xl.p;
       double dl = len(dv);
       if (!(dl > S.eps)) return g;
@@ -917,6 +949,9 @@ Gen generate(Ctx& cx, int tech, int F, const Stream& st, int D) {
       g.xL = xl;
       g.A.v.push_back(xl);
       g.A.v.push_back(vtx_of_hit(xl.p, dir, h));
+      // x_G area-uniform, converted to the solid angle at x_L and then to the area at x_1
+      g.A.pA = {0.0, (1.0 / S.moved_set.area) * dl * dl / std::fabs(dot(xg.n, dir)) * std::fabs(dot(h.tri->n, dir)) /
+                         (h.t * h.t)};
       extend_walk(cx, F, st, g.A, 0, D - 1);
       return g;
     }
@@ -935,6 +970,8 @@ Gen generate(Ctx& cx, int tech, int F, const Stream& st, int D) {
       g.start = xg;
       g.A.v.push_back(E);
       g.A.v.push_back(vtx_of_hit(S.cam_pos, dir, h));
+      g.A.pA = {0.0, (1.0 / S.moved_set.area) * dg * dg / std::fabs(dot(xg.n, dir)) * std::fabs(dot(h.tri->n, dir)) /
+                         (h.t * h.t)};
       extend_walk(cx, F, st, g.A, 0, D - 1);
       return g;
     }
@@ -951,6 +988,10 @@ Gen generate(Ctx& cx, int tech, int F, const Stream& st, int D) {
       if (!hz.ok) return g;
       g.ok = true;
       g.start = xg;
+      // (x_G, d) -> (z_1, y_1): p_A(x_G) p_dir |n_y.d| |n_z.d| / (|n_G.d| |y_1 - z_1|^2), |y_1 - z_1| = t_y + t_z
+      g.pdf0 = (1.0 / S.moved_set.area) * (1.0 / (4.0 * PI)) * std::fabs(dot(hy.tri->n, dir)) *
+               std::fabs(dot(hz.tri->n, dir)) / (std::fabs(dot(xg.n, dir)) * (hy.t + hz.t) * (hy.t + hz.t));
+      g.A.pA = g.B.pA = {0.0, 1.0};
       Vtx y1 = vtx_of_hit(xg.p, dir, hy), z1 = vtx_of_hit(xg.p, dir * -1.0, hz);
       g.B.v.push_back(z1);
       g.B.v.push_back(y1);
@@ -975,6 +1016,8 @@ struct Conn {
   Key key;
   Path path;
   int walk_index;   // single-walk techniques: the walk vertex the connection is made from
+  double pdf_rec = 0;         // product of the densities the generator recorded for this path (C5 pin)
+  int prod_tech = 0, prod_elem = 0;  // the producing candidate: technique and vertex / edge index
 };
 
 // Build every connection path of a generated sample (in its own state)
@@ -983,10 +1026,16 @@ std::vector<Conn> connections(Ctx& cx, const Gen& g, const Stream& st, int D) {
   std::vector<Conn> out;
   if (!g.ok) return out;
   Vtx E = cam_vtx(S);
+  double pL_nee = 0;
   auto nee = [&](int slot) {
     double d[8];
     st.dims((uint32_t)slot, d);
-    return sample_emitter(S, d);
+    return sample_emitter(S, d, &pL_nee);
+  };
+  auto prod = [](const Walk& w, int n) {  // product of the recorded densities of walk vertices 1..n
+    double p = 1.0;
+    for (int m = 1; m <= n; ++m) p *= w.pA[m];
+    return p;
   };
   auto E_rooted = [&](int jmin) {  // T7 / T2 / T5: (E, v_1..v_j, L_j) with NEE slot j
     for (int j = std::max(1, jmin); j <= g.A.n() && j + 1 <= D; ++j) {
@@ -997,6 +1046,9 @@ std::vector<Conn> connections(Ctx& cx, const Gen& g, const Stream& st, int D) {
       for (int m = 1; m <= j; ++m) c.path.x.push_back(g.A.v[m]);
       c.path.x.push_back(nee(j));
       c.path.pixel = g.pixel;
+      c.pdf_rec = g.pdf0 * prod(g.A, j) * pL_nee;
+      c.prod_tech = g.tech;
+      c.prod_elem = g.tech == 2 ? 1 : 0;  // T2: x_D = x_1; T5: the crossing on edge (0, 1); T7: -
       out.push_back(c);
     }
   };
@@ -1009,6 +1061,9 @@ std::vector<Conn> connections(Ctx& cx, const Gen& g, const Stream& st, int D) {
       for (int m = j; m >= 1; --m) c.path.x.push_back(g.A.v[m]);
       c.path.x.push_back(g.xL);
       c.path.pixel = project(S, g.A.v[j].p);
+      c.pdf_rec = g.pdf0 * prod(g.A, j);
+      c.prod_tech = g.tech;
+      c.prod_elem = j;  // T1: x_D = x_{k-2}; T4: the crossing on edge (k-2, k-1)
       out.push_back(c);
     }
   };
@@ -1022,6 +1077,8 @@ std::vector<Conn> connections(Ctx& cx, const Gen& g, const Stream& st, int D) {
         L.kind = K_LIGHT;
         c.path.x = {E, L};
         c.path.pixel = g.pixel;
+        c.pdf_rec = g.pdf0 * g.A.pA[1];
+        c.prod_tech = 7;
         // only an emitter reached directly contributes (C12 #4)
         if (S.emitter_index[L.obj] >= 0) out.push_back(c);
       }
@@ -1053,6 +1110,9 @@ std::vector<Conn> connections(Ctx& cx, const Gen& g, const Stream& st, int D) {
           for (int m = 1; m <= s; ++m) c.path.x.push_back(g.B.v[m]);
           c.path.x.push_back(nee(16 + s));
           c.path.pixel = project(S, g.A.v[t].p);
+          c.pdf_rec = g.pdf0 * prod(g.A, t) * prod(g.B, s) * pL_nee;
+          c.prod_tech = g.tech;
+          c.prod_elem = g.tech == 3 ? t + 1 : t;  // T3: x_D = x_{t+1}; T6: the crossing on edge (t, t+1)
           out.push_back(c);
         }
       }
@@ -1125,7 +1185,8 @@ typedef struct {
   uint64_t seed;
   uint32_t max_depth;
   uint32_t technique_mask;
-  uint32_t flags;  // 1 TWO_WAY, 2 RECONNECT, 4 REJECT_MULTI, 32 VNDF (GGX visible-normal sampling)
+  uint32_t flags;  // 1 TWO_WAY, 2 RECONNECT, 4 REJECT_MULTI, 32 VNDF (GGX visible-normal sampling),
+                   // 64 DIAG_ONE_WAY_ABLATION (one-way with the two-way pairing rules; deliberately biased)
   double jacobian_max, alpha_min, dmin_rel;
 } orc_args;
 
@@ -1156,6 +1217,20 @@ int paired_tech(const Scene& S, int mask, int l) {
   return l;
 }
 
+// R of a reconnected pair (SURVEY 8(c) C7 "R"): the walk-order area pdfs of the mapped suffix in Fbar over
+// those of the base suffix in F, from the reconnection edge v_w -> v_{w+1} to the connection's walk vertex j.
+// The mapped walk is q = (v'_0..v'_w, v_{w+1}..v_j): its prefix from `mapped`, its suffix from `base`.
+double reconnect_R(const Scene& S, int F, const Walk& base, const Walk& mapped, int w, int j) {
+  auto qv = [&](int m) -> const Vtx& { return m <= w ? mapped.v[m] : base.v[m]; };
+  auto pv = [&](int m) -> const Vtx& { return base.v[m]; };
+  double num = 1.0, den = 1.0;
+  for (int m = w + 1; m <= j; ++m) {
+    num *= area_pdf(S, 1 - F, qv(m - 2), qv(m - 1), qv(m));
+    den *= area_pdf(S, F, pv(m - 2), pv(m - 1), pv(m));
+  }
+  return num / den;
+}
+
 struct SampleOut {
   std::vector<orc_record> recs;
 };
@@ -1167,7 +1242,13 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
   const int D = (int)A.max_depth;
   const int F = side, Fb = 1 - side;  // F = 0: new (N); F = 1: old (O)
   const double sigma = side == 0 ? 1.0 : -1.0;
-  const bool two_way = A.flags & 1, reconnect = (A.flags & 2) && two_way, reject_multi = (A.flags & 4) && two_way;
+  // Diagnostic one-way ablation (SURVEY 8(c) C8 last bullet): side N only, N_pix spp samples
+  // per technique, reconnection / rejection as in two-way mode, but a rejected or unpaired base path keeps
+  // weight 1 and paths of O that no N sample maps to are never counted.  It is the estimator P:L425 warns
+  // about ("two-way path mapping to ensure the coverage"): biased by construction, a test mode only.
+  const bool diag = (A.flags & 64) != 0 && !(A.flags & 1);
+  const bool two_way = A.flags & 1, paired = two_way || diag;
+  const bool reconnect = (A.flags & 2) && paired, reject_multi = (A.flags & 4) && paired;
   const double spp = (double)A.spp;
   Stream st{A.seed, i, (uint32_t)l, (uint32_t)side};
   int lq = paired_tech(S, cx.mask, l);
@@ -1320,17 +1401,23 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
             // connection edge: V = 0 zeroes the term, it does not reject
             // R = p_Fbar(suffix | q prefix) / p_F(suffix | p prefix)   (SURVEY 8(c) C7 "R")
             // walk-order vertex m of q: mapped prefix for m <= w, base suffix after
-            auto qv = [&](int m) -> const Vtx& { return m <= w ? gq.A.v[m] : gp.A.v[m]; };
-            auto pv = [&](int m) -> const Vtx& { return gp.A.v[m]; };
-            double num = 1.0, den = 1.0;
-            for (int m = w + 1; m <= j; ++m) {
-              num *= area_pdf(S, Fb, qv(m - 2), qv(m - 1), qv(m));
-              den *= area_pdf(S, F, pv(m - 2), pv(m - 1), pv(m));
-            }
-            R = num / den;
+            R = reconnect_R(S, F, gp.A, gq.A, w, j);
             if (!(R > 0) || !std::isfinite(R)) { status = ST_REJECTED; reason = RJ_TARGET; }
             have_q = status == ST_ACCEPTED;
             if (stats && have_q) stats->reconnected++;
+            if (have_q && cx.recon_out) {  // geometry of the reconnection for the R pins (test export)
+              Walk qw;  // q's walk: mapped prefix, base suffix; R of the inverse map q -> p swaps the roles
+              for (int m = 0; m <= j; ++m) qw.v.push_back(m <= w ? gq.A.v[m] : gp.A.v[m]);
+              double Rinv = reconnect_R(S, Fb, qw, gp.A, w, j);
+              std::vector<double>& o = *cx.recon_out;
+              o.push_back(j - w); o.push_back(R); o.push_back(Rinv);
+              const Vtx* vs[6] = {&gp.A.v[w - 1], &gp.A.v[w], &gq.A.v[w - 1], &gq.A.v[w], &gp.A.v[w + 1],
+                                  j >= w + 2 ? &gp.A.v[w + 2] : &gp.A.v[w + 1]};
+              for (const Vtx* v : vs) {
+                o.push_back(v->p.x); o.push_back(v->p.y); o.push_back(v->p.z);
+                o.push_back(v->n.x); o.push_back(v->n.y); o.push_back(v->n.z);
+              }
+            }
           }
         }
       }
@@ -1361,7 +1448,12 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
     r.status = status;
     r.reason = reason;
     r.R = R;
-    if (two_way) {
+    if (diag) {  // one-way weights with the two-way pairing: accepted +v_N - R v_O, else +v_N (no coverage of O)
+      for (int ch = 0; ch < 3; ++ch) {
+        r.term_p[ch] = vp[ch] / spp;
+        r.term_q[ch] = (status == ST_ACCEPTED) ? -R * vq[ch] / spp : 0.0;
+      }
+    } else if (two_way) {
       double wgt = (status == ST_ACCEPTED) ? 1.0 : 2.0;
       for (int ch = 0; ch < 3; ++ch) {
         r.term_p[ch] = wgt * sigma / spp * vp[ch];
@@ -1389,7 +1481,7 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
     if (recs) recs->push_back(r);
   }
   // one-way mode: every replayed connection of the paired technique contributes -v_O(q)/spp (C8)
-  if (!two_way) {
+  if (!paired) {
     for (const Conn& c : cq) {
       bool used = false;
       for (const Conn* u : used_q)
@@ -1422,11 +1514,14 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
 // ------------------------------------------------------------------------------------------------
 // primal renderer: unidirectional PT with NEE + BSDF sampling combined by the balance heuristic
 // (an estimator independent of the residual code path).  Paths with <= D edges.
-// Streams: counter (pixel-sample index lo/hi, 0x100 + F, 2*vertex + call), key = seed.
+// Streams: counter (pixel-sample index lo/hi, 0x80 | stream_state << 8, 2*vertex + call), key = seed; the
+// stream state is F by default (independent streams per state).  With the same stream state for both
+// states the two images use the same random numbers, so their difference is a correlated (low-variance)
+// but still unbiased estimate of I^D(N) - I^D(O): the reference of the convergence pins.
 // ------------------------------------------------------------------------------------------------
-void primal_pixel_sample(Ctx& cx, int F, uint64_t seed, uint64_t idx, int D, double* img) {
+void primal_pixel_sample(Ctx& cx, int F, uint64_t seed, uint64_t idx, int D, double* img, int stream_state) {
   const Scene& S = *cx.S;
-  Stream st{seed, idx, 0x80u, (uint32_t)F};  // technique id 0x80 is never used by the residual streams
+  Stream st{seed, idx, 0x80u, (uint32_t)stream_state};  // technique id 0x80 is never used by the residual streams
   int npix = S.W * S.H;
   int pix = (int)(idx % (uint64_t)npix);
   double d0[8];
@@ -1681,18 +1776,93 @@ int orc_residual(void* h, const orc_args* A, int tech, int side, uint64_t i0, ui
 }
 
 // Primal render of state F (0 = N, 1 = O): samples idx in [i0, i1) (pixel = idx mod N_pix).
-int orc_primal(void* h, int F, uint64_t seed, int D, uint64_t i0, uint64_t i1, double* img, orc_stats* stats) {
+int orc_primal_streams(void* h, int F, int stream_state, uint64_t seed, int D, uint64_t i0, uint64_t i1, double* img,
+                       orc_stats* stats) {
   Oracle* O = (Oracle*)h;
   O->S.vndf = false;  // the primal renderer samples GGX from D(h) |n.h|
   Ctx cx;
   cx.S = &O->S;
   cx.mask = 0x7F;
-  for (uint64_t i = i0; i < i1; ++i) primal_pixel_sample(cx, F, seed, i, D, img);
+  for (uint64_t i = i0; i < i1; ++i) primal_pixel_sample(cx, F, seed, i, D, img, stream_state);
   if (stats) {
     stats->closest_rays += cx.C.closest;
     stats->shadow_rays += cx.C.shadow;
   }
   return 0;
+}
+int orc_primal(void* h, int F, uint64_t seed, int D, uint64_t i0, uint64_t i1, double* img, orc_stats* stats) {
+  return orc_primal_streams(h, F, F, seed, D, i0, i1, img, stats);
+}
+
+// Technique-pdf self-consistency: for every connection of the base samples [i0, i1)
+// of (tech, side), the product of the densities the generator recorded while sampling the path, and the
+// technique pdf eval_path assigns to the producing candidate (C5 table; for T4-T6 the crossing at x_G).
+// out: 3 doubles per connection {recorded, eval_path candidate pdf (-1: producer not among the
+// candidates), #candidates}.  Returns the number of connections (up to cap written).
+int64_t orc_pdf_check(void* h, const orc_args* A, int tech, int side, uint64_t i0, uint64_t i1, double* out,
+                      int64_t cap) {
+  Oracle* O = (Oracle*)h;
+  O->S.vndf = (A->flags & 32u) != 0;
+  const Scene& S = O->S;
+  Ctx cx;
+  cx.S = &S;
+  cx.mask = effective_mask(S, A->technique_mask);
+  int64_t n = 0;
+  for (uint64_t i = i0; i < i1; ++i) {
+    Stream st{A->seed, i, (uint32_t)tech, (uint32_t)side};
+    Gen g = generate(cx, tech, side, st, (int)A->max_depth);
+    for (const Conn& c : connections(cx, g, st, (int)A->max_depth)) {
+      Eval ev = eval_path(cx, side, c.path, false);
+      double pc = -1.0;
+      int k = (int)c.path.x.size();
+      for (size_t a = 0; a < ev.cands.size(); ++a) {
+        const Cand& cd = ev.cands[a];
+        if (cd.tech != c.prod_tech) continue;
+        if (c.prod_tech == 7) { pc = ev.cand_p[a]; break; }
+        int elem = c.prod_tech == 1 ? k - 2 : (c.prod_tech == 4 ? k - 2 : c.prod_elem);
+        if (cd.elem != elem) continue;
+        if (c.prod_tech >= 4 && c.prod_tech <= 6) {  // the crossing through x_G
+          if (len(ev.cross[cd.elem][cd.sub].p - g.start.p) > 1e-6 * S.diag) continue;
+        }
+        pc = ev.cand_p[a];
+        break;
+      }
+      if (n < cap) {
+        out[3 * n] = c.pdf_rec;
+        out[3 * n + 1] = pc;
+        out[3 * n + 2] = (double)ev.cands.size();
+      }
+      n++;
+    }
+  }
+  return n;
+}
+
+// Accepted reconnections of the samples [i0, i1) of (tech, side) (test export for the R pins, SURVEY 8(c)
+// C11): 39 doubles each = {j - w, R, R of the inverse map q -> p, then (position, normal) of v_{w-1}, v_w,
+// v'_{w-1}, v'_w, v_{w+1}, v_{w+2} (= v_{w+1} when j = w + 1)}.  Returns the number of reconnections.
+int64_t orc_reconnections(void* h, const orc_args* A, int tech, int side, uint64_t i0, uint64_t i1, double* out,
+                          int64_t cap) {
+  Oracle* O = (Oracle*)h;
+  O->S.vndf = (A->flags & 32u) != 0;
+  Ctx cx;
+  cx.S = &O->S;
+  cx.mask = effective_mask(O->S, A->technique_mask);
+  if (!((cx.mask >> 6) & 1)) return -1;
+  std::vector<double> rec;
+  cx.recon_out = &rec;
+  std::vector<double> img(3 * (size_t)O->S.W * O->S.H, 0.0);
+  for (uint64_t i = i0; i < i1; ++i) residual_sample(cx, *A, tech, side, i, img.data(), nullptr, nullptr);
+  int64_t n = (int64_t)(rec.size() / 39);
+  std::memcpy(out, rec.data(), sizeof(double) * 39 * (size_t)std::min(n, cap));
+  return n;
+}
+
+// T3's emitter-side start direction for normal n and slot-0 dims (u3, u4): out = {w, recorded pdf}
+void orc_t3_light_dir(const double n[3], double u3, double u4, double out[4]) {
+  double pdf;
+  V3 w = t3_light_dir(v3(n[0], n[1], n[2]), u3, u4, &pdf);
+  out[0] = w.x; out[1] = w.y; out[2] = w.z; out[3] = pdf;
 }
 
 // debug: print the base / mapped connection paths of one sample

@@ -10,13 +10,4 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
-    config.addinivalue_line("markers", "slow: long statistical test; enabled with RR_SLOW=1")
 
-
-def pytest_collection_modifyitems(config, items):
-    if os.environ.get("RR_SLOW") == "1":
-        return
-    skip = pytest.mark.skip(reason="slow statistical test (set RR_SLOW=1)")
-    for it in items:
-        if "slow" in it.keywords:
-            it.add_marker(skip)

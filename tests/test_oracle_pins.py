@@ -1,0 +1,273 @@
+"""Pins of the oracle's residual estimator that SURVEY 8(c) C11 lists beyond the closed forms of
+test_oracle_units / test_oracle_estimator: each compares the oracle against something other than itself.
+
+  * technique-pdf self-consistency (C5): the densities the generator records while it samples a path
+    multiply to the technique pdf eval_path assigns to the producing candidate;
+  * R (C7 "R"): R of the inverse map is 1/R; on Lambert geometry R equals the paper's reconnection Jacobian
+    (Eq. P:L397-401) times the ratio of the cosine pdfs at the reconnecting vertices, written out here in numpy;
+  * T3's direction density cos(theta)/pi (golden value) and the area density 1/A;
+  * convergence: the residual's mean agrees with I^D(N) - I^D(O) from the independent primal
+    renderer (correlated streams, unbiased) and its MSE falls as 1/spp (log-log slope -1 +- 0.15);
+  * two-way necessity: the one-way ablation with the pairing rules is biased and plateaus;
+  * swap antisymmetry: E[Delta(A -> B)] = -E[Delta(B -> A)].
+"""
+import dataclasses
+import json
+import math
+import multiprocessing as mp
+import os
+
+import numpy as np
+import pytest
+
+from oracle import binding as B
+from rr_inputs import scenes as S
+
+VALS = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
+DIAG = 64  # RR_DIAG_ONE_WAY_ABLATION
+
+
+def _pool():
+    return mp.get_context("fork").Pool(min(8, mp.cpu_count()))
+
+
+# ---------------------------------------------------------------- technique pdfs (C5)
+@pytest.mark.parametrize("fixture,flags", [("c1", S.PAPER_FLAGS), ("rev", S.PAPER_FLAGS), ("c2", S.PAPER_FLAGS),
+                                           ("c2", S.PAPER_FLAGS | S.VNDF)])
+def test_technique_pdf_self_consistency(fixture, flags):
+    """For every connection of every technique, the product of the densities the generator recorded (film
+    point, BSDF directions with their hit distances, x_D / x_G / x_L / T6 line densities) equals the C5
+    technique pdf of the producing candidate computed by eval_path from the vertices."""
+    w = {"c1": lambda: S.config1(16, 16, spp=4, max_depth=6), "rev": lambda: S.occluder_reveal(16, 16, 4, 6),
+         "c2": lambda: S.config2(32, 32, spp=4, max_depth=6)}[fixture]()
+    o = B.Oracle(w.scene, w.edits)
+    args = dataclasses.replace(w.args, flags=flags)
+    mask = o.effective_mask(0x7F)
+    seen = set()
+    for l in range(1, 8):
+        if not (mask >> (l - 1)) & 1:
+            continue
+        for side in (0, 1):
+            r = o.pdf_check(args, l, side, 0, 1500)
+            if len(r) == 0:
+                continue
+            seen.add(l)
+            assert np.all(r[:, 2] > 0)            # every path is a camera path with >= 1 candidate
+            assert np.all(r[:, 1] >= 0), l        # the producer is always among the candidates
+            rel = np.abs(r[:, 0] - r[:, 1]) / np.abs(r[:, 1])
+            assert rel.max() <= 1e-11, (l, side, rel.max())
+            assert np.quantile(rel, 0.999) <= 1e-12, (l, side)
+    assert seen == {l for l in range(1, 8) if (mask >> (l - 1)) & 1}
+
+
+# ---------------------------------------------------------------- R (C7)
+def _unit(v):
+    return v / np.linalg.norm(v, axis=-1, keepdims=True)
+
+
+def test_R_of_inverse_map_is_reciprocal():
+    w = S.config1(32, 32, spp=4, max_depth=6)
+    o = B.Oracle(w.scene, w.edits)
+    n = 0
+    for l in (1, 2, 4, 5, 7):
+        for side in (0, 1):
+            r = o.reconnections(w.args, l, side, 0, 3000)
+            n += len(r)
+            if len(r):
+                np.testing.assert_allclose(r[:, 1] * r[:, 2], 1.0, rtol=1e-13)
+    assert n > 2000
+
+
+def test_R_lambert_equals_paper_jacobian_times_cosine_ratio():
+    """All-Lambert scene (config 1): R = J (Eq. P:L397-401, at the target v_{w+1}) x cos(v'_w)/cos(v_w), the
+    ratio of the cosine pdfs of the reconnection edge at the two diverged vertices; the factor of the next
+    edge is 1 because a Lambert target's pdf does not depend on the incoming direction."""
+    w = S.config1(32, 32, spp=4, max_depth=6)
+    o = B.Oracle(w.scene, w.edits)
+    rows = np.concatenate([o.reconnections(w.args, l, s, 0, 3000) for l in (1, 2, 4, 5, 7) for s in (0, 1)])
+    assert len(rows) > 2000 and np.any(rows[:, 0] >= 2)  # both R1 alone and R1 * R2 appear
+    P = rows[:, 3:].reshape(-1, 6, 6)
+    vw, nw, vq, nq, t, nt = P[:, 1, :3], P[:, 1, 3:], P[:, 3, :3], P[:, 3, 3:], P[:, 4, :3], P[:, 4, 3:]
+    a, b = vq - t, vw - t  # from the target toward v'_w and v_w
+    J = np.abs((nt * _unit(a)).sum(1)) / np.abs((nt * _unit(b)).sum(1)) * (b * b).sum(1) / (a * a).sum(1)
+    cos_q = np.abs((nq * _unit(t - vq)).sum(1))
+    cos_p = np.abs((nw * _unit(t - vw)).sum(1))
+    np.testing.assert_allclose(rows[:, 1], J * cos_q / cos_p, rtol=1e-10)
+    # the paper's rejection band [1/10, 10] applies to J: every accepted reconnection lies inside
+    assert np.all((J <= 10 * (1 + 1e-12)) & (J >= 0.1 * (1 - 1e-12)))
+
+
+# ---------------------------------------------------------------- samplers with golden values
+def test_area_pdf_single_triangle_golden():
+    """area-uniform sampling of one triangle of area 2 has pdf 1/2."""
+    b = S._Builder()
+    m = b.material(S.Material(S.LAMBERT, (0.5, 0.5, 0.5)))
+    b.add(*S.quad((-5, 3, -5), (10, 0, 0), (0, 0, 10)), m, emission=(1.0, 1.0, 1.0))
+    tri = (np.array([[0, 0, 0], [2, 0, 0], [0, 0, 2]], np.float32), np.array([[0, 2, 1]], np.uint32))
+    obj = b.add(*tri, m, flags=S.OBJ_DYNAMIC)
+    scene = b.build(S.Camera((0.0, 1.0, -3.0), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 60.0, 8, 8), 1e-4, "one-tri")
+    eye = S.translate_xform((0.0, 0.0, 0.0))
+    o = B.Oracle(scene, [S.Edit(obj, eye, eye.copy())])
+    assert 1.0 / o.set_area(0) == pytest.approx(VALS["area_pdf"]["single_triangle_area_2"], rel=1e-12)
+    rng = np.random.default_rng(4)
+    pts = np.array([o.sample_set(0, 0, *rng.random(3))[:3] for _ in range(20000)])
+    # uniform density on the triangle x, z >= 0, x + z <= 2: E[x] = E[z] = 2/3, P(x < 1, z < 1) = 1/2
+    assert abs(pts[:, 0].mean() - 2 / 3) < 0.02 and abs(pts[:, 2].mean() - 2 / 3) < 0.02
+    assert abs(((pts[:, 0] < 1) & (pts[:, 2] < 1)).mean() - 0.5) < 0.015
+
+
+def test_t3_direction_pdf_is_cos_over_pi():
+    """S:L241 / P:L301: T3's emitter-side start direction is cosine-weighted about +n; the density the
+    generator records is cos(theta)/pi, and cos^2(theta) of the samples is uniform on [0, 1]."""
+    assert VALS["t3_direction_pdf"]["cos_theta_over_pi"] is True
+    rng = np.random.default_rng(5)
+    n = _unit(np.array([0.3, -0.5, 0.8]))
+    c2 = []
+    for u3, u4 in rng.random((20000, 2)):
+        wv, pdf = B.t3_light_dir(n, u3, u4)
+        c = float(np.dot(wv, n))
+        assert c >= 0 and pdf == pytest.approx(c / math.pi, rel=1e-12, abs=1e-15)
+        c2.append(c * c)
+    h = np.histogram(c2, bins=20, range=(0, 1))[0]
+    chi = ((h - 1000) ** 2 / 1000).sum()
+    assert chi < 43.8  # p = 0.001, 19 dof
+
+
+# ---------------------------------------------------------------- convergence and the MSE slope
+def _fixture(name, spp=16):
+    if name == "c1":
+        return S.load_config(1, width=8, height=8, spp=spp, max_depth=4)
+    if name == "rev":
+        return S.occluder_reveal(8, 8, spp, 4)
+    return S.load_config(2, width=8, height=8, spp=spp, max_depth=4)
+
+
+def _res_chunk(a):
+    name, seed, flags = a
+    w = _fixture(name)
+    o = B.Oracle(w.scene, w.edits)
+    return o.render_residual(dataclasses.replace(w.args, seed=seed, flags=flags))[0]
+
+
+def _ref_chunk(a):
+    name, seed = a
+    w = _fixture(name)
+    return B.Oracle(w.scene, w.edits).primal_difference(seed, 1024, 4)
+
+
+_CACHE = {}
+
+
+def _runs(name, flags_list, n_chunks=128, n_ref=128):
+    key = (name, tuple(flags_list))
+    if key not in _CACHE:
+        with _pool() as p:
+            ref = np.stack(p.map(_ref_chunk, [(name, 10000 + s) for s in range(n_ref)]))
+            res = {f: np.stack(p.map(_res_chunk, [(name, s, f) for s in range(n_chunks)])) for f in flags_list}
+        _CACHE[key] = (ref, res)
+    return _CACHE[key]
+
+
+def _bias_z(chunks, ref):
+    m, sm = chunks.mean(0), chunks.std(0) / math.sqrt(len(chunks))
+    d, sd = ref.mean(0), ref.std(0) / math.sqrt(len(ref))
+    var = sm ** 2 + sd ** 2 + 1e-300
+    z = (m - d) / np.sqrt(var)
+    tot = (m - d).sum((0, 1)) / np.sqrt(var.sum((0, 1)))
+    return z, tot
+
+
+def _mse_curve(chunks, ref, levels=(1, 4, 16, 64)):
+    """MSE against the reference at 16 x g spp (groups of g chunks), minus the reference's own variance"""
+    d = ref.mean(0)
+    var_d = (ref.var(0) / len(ref)).mean()
+    out = []
+    for g in levels:
+        est = chunks[: (len(chunks) // g) * g].reshape(-1, g, *chunks.shape[1:]).mean(1)
+        out.append(((est - d) ** 2).mean() - var_d)
+    return np.array(out)
+
+
+def _slope(levels, mse):
+    return np.polyfit(np.log(16 * np.array(levels)), np.log(mse), 1)[0]
+
+
+@pytest.mark.parametrize("name", ["c1", "rev", "c2"])
+def test_residual_converges_to_primal_difference(name):
+    """Mean of 128 independent 16-spp residual renders (paper mode, and two-way replay only) vs
+    I^D(N) - I^D(O) from the primal NEE/BSDF-MIS renderer at 128 x 1024 spp: per-pixel z
+    scores are consistent with N(0, 1) (sum of z^2 within 5 sd of its chi-square mean, >= 97% of |z| < 3, the
+    image sums within 4 sd), and the MSE falls as 1/spp over 16..1024 spp (slope -1 +- 0.15)."""
+    ref, res = _runs(name, (S.PAPER_FLAGS, S.TWO_WAY))
+    levels = (1, 4, 16, 64)
+    for flags, chunks in res.items():
+        z, tot = _bias_z(chunks, ref)
+        n = z.size
+        assert (z ** 2).sum() < n + 5 * math.sqrt(2 * n), (flags, (z ** 2).sum())
+        assert (np.abs(z) < 3).mean() >= 0.97, flags
+        assert np.all(np.abs(tot) < 4), (flags, tot)
+        mse = _mse_curve(chunks, ref, levels)
+        assert np.all(mse > 0)
+        sl = _slope(levels, mse)
+        assert abs(sl + 1) <= 0.15, (flags, sl, mse)
+
+
+@pytest.mark.parametrize("name", ["c1", "rev"])
+def test_two_way_necessity(name):
+    """P:L425 ("two-way path mapping to ensure the coverage"): the one-way estimator with the same
+    pairing / rejection rules (RR_DIAG_ONE_WAY_ABLATION: rejected base paths keep weight 1, O paths no N
+    sample maps to are never counted) converges to the wrong image -- its error plateaus -- while the
+    two-way estimator on the same fixture keeps the 1/spp slope (test above)."""
+    ref, res = _runs(name, (S.PAPER_FLAGS, DIAG | S.RECONNECT | S.REJECT_MULTI))
+    one = res[DIAG | S.RECONNECT | S.REJECT_MULTI]
+    z, tot = _bias_z(one, ref)
+    assert np.all(np.abs(tot) > 10), tot                      # biased
+    levels = (1, 4, 16, 64)
+    mse = _mse_curve(one, ref, levels)
+    assert mse[-1] > 0.25 * mse[-2], mse                      # plateau: 4x the samples, < 2x less error
+    assert _slope(levels[2:], mse[2:]) > -0.5
+    two = _mse_curve(res[S.PAPER_FLAGS], ref, levels)
+    assert two[-1] < 0.1 * mse[-1]
+
+
+def test_one_way_ablation_equals_two_way_without_rejections():
+    """With nothing rejected or unpaired the diagnostic mode is plain one-way replay: on the identity edit both
+    are exactly zero, and on a Lambert albedo edit (never diverges) its records are those of flags 0."""
+    w = S.cornell_albedo_scale(0.5, 12, 12, spp=4)
+    o = B.Oracle(w.scene, w.edits)
+    a, ra, _ = o.render_residual(dataclasses.replace(w.args, flags=DIAG | S.RECONNECT | S.REJECT_MULTI), records=True)
+    b, rb, _ = o.render_residual(dataclasses.replace(w.args, flags=0), records=True)
+    np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-15)
+    assert len(ra) == len(rb) > 100 and all(r.status == 0 for r in ra)
+
+
+# ---------------------------------------------------------------- swap antisymmetry
+def _swap(w):
+    e = [dataclasses.replace(x, old_xform=x.new_xform, new_xform=x.old_xform, old_material=x.new_material,
+                             new_material=x.old_material) for x in w.edits]
+    return dataclasses.replace(w, edits=e)
+
+
+def _swap_chunk(a):
+    name, seed, swapped = a
+    w = _fixture(name)
+    if swapped:
+        w = _swap(w)
+    o = B.Oracle(w.scene, w.edits)
+    return o.render_residual(dataclasses.replace(w.args, seed=seed))[0]
+
+
+@pytest.mark.parametrize("name", ["c1", "rev", "c2"])
+def test_swap_antisymmetry(name):
+    """Exchanging the two states negates the residual in expectation: E[Delta(A -> B)] = -E[Delta(B -> A)]
+    (Eq.4; the techniques, mapping and rejection rules are symmetric in the two states)."""
+    with _pool() as p:
+        f = np.stack(p.map(_swap_chunk, [(name, s, False) for s in range(64)]))
+        b = np.stack(p.map(_swap_chunk, [(name, 5000 + s, True) for s in range(64)]))
+    m = f.mean(0) + b.mean(0)
+    var = f.var(0) / 64 + b.var(0) / 64 + 1e-300
+    z = m / np.sqrt(var)
+    assert (z ** 2).sum() < z.size + 5 * math.sqrt(2 * z.size), (z ** 2).sum()
+    tot = m.sum((0, 1)) / np.sqrt(var.sum((0, 1)))
+    assert np.all(np.abs(tot) < 4), tot
+    assert np.abs(f.mean(0)).max() > 10 * np.sqrt(var).max()  # the residual itself is far from 0
