@@ -98,9 +98,15 @@ enum {
   RR_REJECT_MULTI = 4u,/* reject diverged pairs with >= 2 dynamic vertices; requires RR_TWO_WAY */
   RR_ACCUMULATE = 8u,  /* add into d_image instead of overwriting it */
   RR_COUNT_TRAVERSAL = 16u,/* count BVH node fetches / triangle tests into rr_stats (diagnostic, ~3% slower) */
-  RR_VNDF = 32u            /* sample GGX directions from the visible normals of the incoming direction (Heitz
+  RR_VNDF = 32u,           /* sample GGX directions from the visible normals of the incoming direction (Heitz
                               2018) instead of D(h)|n.h|; pdfs and MIS follow.  A variance-only variant
                               (SURVEY 8(f) row 4); residual renders only (the primal renderer ignores it) */
+  RR_DIAG_ONE_WAY_ABLATION = 64u /* DIAGNOSTIC, deliberately biased: one-way
+                              (side N only, N_pix*spp samples per technique, RR_TWO_WAY must be off) but with the
+                              two-way pairing rules (RR_RECONNECT / RR_REJECT_MULTI allowed); accepted pairs splat
+                              +v_N(p) - R v_O(q), rejected / unpaired base paths +v_N(p) with weight 1, and O paths
+                              that no N sample maps to are never counted.  The estimator P:L425 warns against
+                              ("two-way path mapping to ensure the coverage"); the two-way-necessity test mode. */
 };
 #define RR_PAPER_FLAGS (RR_TWO_WAY | RR_RECONNECT | RR_REJECT_MULTI)
 #define RR_MAX_DEPTH 10
@@ -111,7 +117,8 @@ typedef struct {
   uint32_t max_depth;      /* D = max number of path edges, 1..RR_MAX_DEPTH (C12 #1) */
   uint32_t technique_mask; /* bit l-1 enables technique l (T1..T7); must contain T7 (bit 6) */
   uint32_t flags;          /* RR_* flags above; RR_PAPER_FLAGS = the paper's method; mask 0x40 + flags 0 =
-                              correlated PT */
+                              correlated PT.  RR_RECONNECT / RR_REJECT_MULTI need RR_TWO_WAY or
+                              RR_DIAG_ONE_WAY_ABLATION; the latter excludes RR_TWO_WAY (RR_E_INVALID otherwise) */
   float jacobian_max;      /* 10 */
   float alpha_min;         /* roughness threshold, 0.1 */
   float dmin_rel;          /* distance threshold / scene diagonal, 0.01 */

@@ -680,9 +680,12 @@ static rr_status check_args(rr_ctx* c, const rr_render_args* a) {
   if (!(a->technique_mask & 0x40u)) return fail(c, RR_E_INVALID, "technique mask must contain T7");
   if (a->technique_mask & ~0x7Fu) return fail(c, RR_E_INVALID, "unknown technique bits");
   if (a->layer_mask & ~0x7Fu) return fail(c, RR_E_INVALID, "unknown layer bits");
-  if (!(a->flags & RR_TWO_WAY) && (a->flags & (RR_RECONNECT | RR_REJECT_MULTI)))
-    return fail(c, RR_E_INVALID, "RR_RECONNECT / RR_REJECT_MULTI require RR_TWO_WAY");
-  if (a->flags & ~(RR_TWO_WAY | RR_RECONNECT | RR_REJECT_MULTI | RR_ACCUMULATE | RR_COUNT_TRAVERSAL | RR_VNDF))
+  if (!(a->flags & (RR_TWO_WAY | RR_DIAG_ONE_WAY_ABLATION)) && (a->flags & (RR_RECONNECT | RR_REJECT_MULTI)))
+    return fail(c, RR_E_INVALID, "RR_RECONNECT / RR_REJECT_MULTI require RR_TWO_WAY (or RR_DIAG_ONE_WAY_ABLATION)");
+  if ((a->flags & RR_TWO_WAY) && (a->flags & RR_DIAG_ONE_WAY_ABLATION))
+    return fail(c, RR_E_INVALID, "RR_DIAG_ONE_WAY_ABLATION is one-way: RR_TWO_WAY must be off");
+  if (a->flags & ~(RR_TWO_WAY | RR_RECONNECT | RR_REJECT_MULTI | RR_ACCUMULATE | RR_COUNT_TRAVERSAL | RR_VNDF |
+                   RR_DIAG_ONE_WAY_ABLATION))
     return fail(c, RR_E_INVALID, "unknown flag bits");
   if (a->shard_count == 0 || a->shard_index >= a->shard_count) return fail(c, RR_E_INVALID, "bad shard");
   return RR_OK;
@@ -707,7 +710,10 @@ static KArgs make_kargs(rr_ctx* c, const rr_render_args* a, uint32_t mask, int l
   K.side = side;
   K.max_depth = (int)a->max_depth;
   K.mask = mask;
-  K.two_way = (a->flags & RR_TWO_WAY) ? 1 : 0;
+  // paired control flow (no mapped-only partner terms; reconnection / rejection allowed) in two-way mode and in
+  // the diagnostic one-way ablation; the ablation changes the weights only (rr_shade.cuh finish)
+  K.two_way = (a->flags & (RR_TWO_WAY | RR_DIAG_ONE_WAY_ABLATION)) ? 1 : 0;
+  K.diag = (a->flags & RR_DIAG_ONE_WAY_ABLATION) ? 1 : 0;
   K.count = (a->flags & RR_COUNT_TRAVERSAL) ? 1 : 0;
   K.mat_type_vndf = (a->flags & RR_VNDF) ? c->mat_type_vndf.p : nullptr;
   K.reconnect = (a->flags & RR_RECONNECT) ? 1 : 0;
@@ -719,7 +725,7 @@ static KArgs make_kargs(rr_ctx* c, const rr_render_args* a, uint32_t mask, int l
   K.alpha_min = a->alpha_min;
   K.dmin = (float)(a->dmin_rel * c->diag);
   uint64_t npix = (uint64_t)c->cam.width * c->cam.height;
-  K.n_total = K.two_way ? npix * a->spp / 2 : npix * a->spp;
+  K.n_total = (a->flags & RR_TWO_WAY) ? npix * a->spp / 2 : npix * a->spp;
   K.shard_index = a->shard_index;
   K.shard_count = a->shard_count;
   uint64_t nb = (K.n_total + 0xFFFF) >> 16;

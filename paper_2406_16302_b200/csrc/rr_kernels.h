@@ -17,7 +17,8 @@ enum {
 struct KArgs {
   int tech, tech_q, side, max_depth;
   uint32_t mask;
-  int two_way, reconnect, reject_multi;
+  int two_way, reconnect, reject_multi;  // two_way: paired control flow (RR_TWO_WAY or the diagnostic ablation)
+  int diag;                              // RR_DIAG_ONE_WAY_ABLATION weights
   uint64_t seed;
   float sigma, inv_spp, jacobian_max, alpha_min, dmin;
   uint64_t n_total;                  // samples of this (technique, side) over all shards

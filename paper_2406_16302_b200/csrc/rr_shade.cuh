@@ -234,7 +234,11 @@ __device__ inline void finish(Out& o, uint64_t i, int kind, int a, int b, int st
                        int pix_q, float3 vq, float R) {
   const KArgs& A = *o.A;
   float3 tp, tq;
-  if (A.two_way) {
+  if (A.diag) {  // diagnostic one-way ablation: weight 1 for every base term, the partner only when accepted
+    tp = vp * A.inv_spp;
+    tq = (status == ST_ACCEPTED) ? vq * (-A.inv_spp * R) : f3(0.f, 0.f, 0.f);
+    if (status != ST_ACCEPTED) pix_q = -1;
+  } else if (A.two_way) {
     float wgt = (status == ST_ACCEPTED) ? 1.0f : 2.0f;
     tp = vp * (wgt * A.sigma * A.inv_spp);
     tq = (status == ST_ACCEPTED) ? vq * (-A.sigma * A.inv_spp * R) : f3(0.f, 0.f, 0.f);

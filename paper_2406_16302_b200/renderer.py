@@ -230,7 +230,3 @@ class Renderer:
                                       torch.cuda.current_stream(self.device).cuda_stream), "rr_philox")
         return out
 
-
-def sample_count(width: int, height: int, args) -> int:
-    """Residual samples per render = (#enabled techniques) x N_pix x spp."""
-    return width * height * int(args.spp)

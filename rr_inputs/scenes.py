@@ -37,6 +37,7 @@ REJECT_MULTI = 4
 ACCUMULATE = 8
 PAPER_FLAGS = TWO_WAY | RECONNECT | REJECT_MULTI
 VNDF = 32  # GGX directions from the visible normals (Heitz 2018), both implementations
+DIAG_ONE_WAY = 64  # RR_DIAG_ONE_WAY_ABLATION: one-way with the two-way pairing rules (biased test mode)
 
 
 @dataclasses.dataclass

@@ -78,20 +78,39 @@ def compare_records(grecs, orecs):
     return len(keys), ok, bad
 
 
-def record_parity(w, args, n_per=None, min_frac=0.999, techniques=None):
+def strided_ranges(n_total, n_per, chunk=128, seed=0):
+    """index ranges [i0, i1) of about n_per indices in chunks of `chunk` at seeded random positions over the
+    WHOLE index range of a (technique, side), so that T7's pixel i mod N_pix covers every image row and every
+    spp pass"""
+    if n_per >= n_total:
+        return [(0, n_total)]
+    k = max(1, n_per // chunk)
+    starts = np.sort(np.random.default_rng(seed).choice(n_total // chunk, size=k, replace=False)) * chunk
+    return [(int(a), int(min(a + chunk, n_total))) for a in starts]
+
+
+def record_parity(w, args, n_per=None, min_frac=0.999, techniques=None, strided=False):
     r = _renderer(w)
     o = _oracle(w)
     mask = o.effective_mask(args.technique_mask)
-    n = o.sample_range(args) if n_per is None else min(n_per, o.sample_range(args))
-    sides = (0, 1) if (args.flags & 1) else (0,)
+    n_all = o.sample_range(args)
+    if n_per is None:
+        ranges = [(0, n_all)]
+    elif strided:
+        ranges = strided_ranges(n_all, n_per)
+    else:
+        ranges = [(0, min(n_per, n_all))]
+    sides = o.sides(args)
     total = good = 0
     allbad = []
     for l in range(1, 8):
         if not (mask >> (l - 1)) & 1 or (techniques and l not in techniques):
             continue
         for s in sides:
-            g = r.dump_paths(args, l, s, 0, n)
-            _, orc, _ = o.residual(args, l, s, 0, n, records=True)
+            g, orc = [], []
+            for i0, i1 in ranges:
+                g += r.dump_paths(args, l, s, i0, i1)
+                orc += o.residual(args, l, s, i0, i1, records=True)[1]
             t, k, bad = compare_records(g, orc)
             total += t
             good += k
@@ -263,10 +282,25 @@ def test_records_occluder_reveal(torch_cuda):
 
 @pytest.mark.parametrize("cfg", [3, 4, 5])
 def test_records_full_size_configs_sampled(torch_cuda, cfg):
-    """Full BASELINE sizes (scene, camera, resolution, D) -- the first indices of every (technique,
-    side), computed one by one by the oracle.  Config 5: frame 0 of the animation (3 moved objects)."""
+    """Full BASELINE sizes (scene, camera, resolution, D) -- ~3000 indices of every (technique, side) in
+    chunks spread over its WHOLE index range (every image row and spp pass; the moved object at the image
+    centre included), computed one by one by the oracle.  Config 5: frame 0 (3 moved objects)."""
     w = S.load_config(cfg)
-    record_parity(w, w.args, n_per=3000 if cfg != 5 else 2000)
+    record_parity(w, w.args, n_per=3072 if cfg != 5 else 2048, strided=True)
+
+
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_records_full_size_diag_one_way(torch_cuda, cfg):
+    """RR_DIAG_ONE_WAY_ABLATION (the biased test mode of the two-way-necessity pin) at full size, strided."""
+    w = S.load_config(cfg)
+    args = dataclasses.replace(w.args, flags=S.DIAG_ONE_WAY | S.RECONNECT | S.REJECT_MULTI)
+    record_parity(w, args, n_per=1024, strided=True)
+
+
+def test_records_diag_one_way_config1(torch_cuda):
+    w = S.config1()
+    args = dataclasses.replace(w.args, flags=S.DIAG_ONE_WAY | S.RECONNECT | S.REJECT_MULTI)
+    record_parity(w, args)
 
 
 def test_records_config5_late_frame(torch_cuda):
@@ -274,7 +308,7 @@ def test_records_config5_late_frame(torch_cuda):
     w = S.config5()
     f = 11
     w = dataclasses.replace(w, edits=w.frames[f], args=dataclasses.replace(w.args, seed=w.args.seed + f))
-    record_parity(w, w.args, n_per=1000)
+    record_parity(w, w.args, n_per=1024, strided=True)
 
 
 def test_config5_chain_is_sum_of_frames(torch_cuda):
@@ -294,35 +328,75 @@ def test_config5_chain_is_sum_of_frames(torch_cuda):
 
 
 # ---------------------------------------------------------------- images and exact special cases
+def _image_workload(cfg, W, H, spp, D=None, seed=None):
+    w = S.load_config(cfg, width=W, height=H, spp=spp, **({} if D is None else {"max_depth": D}))
+    if seed is not None:
+        w = dataclasses.replace(w, args=dataclasses.replace(w.args, seed=seed))
+    return w
+
+
 def _oracle_image(a):
-    cfg, W, spp, D, seed, t0, t1 = a
+    """one slice (t0 of nt) of every (technique, side) index range, on a host core"""
+    key, t0, nt = a
     from oracle import binding as OB
-    w = S.load_config(cfg, width=W, height=W, spp=spp, max_depth=D)
-    args = dataclasses.replace(w.args, seed=seed)
+    w = _image_workload(*key)
     o = OB.Oracle(w.scene, w.edits)
-    img = np.zeros((W, W, 3))
-    n = o.sample_range(args)
-    mask = o.effective_mask(args.technique_mask)
+    img = np.zeros((o.H, o.W, 3))
+    n = o.sample_range(w.args)
+    mask = o.effective_mask(w.args.technique_mask)
     for l in range(1, 8):
         if (mask >> (l - 1)) & 1:
-            for s in (0, 1):
-                o.residual(args, l, s, n * t0 // 8, n * t1 // 8, image=img)
+            for s in o.sides(w.args):
+                o.residual(w.args, l, s, n * t0 // nt, n * (t0 + 1) // nt, image=img)
     return img
 
 
-def test_image_rmse_config1(torch_cuda):
-    torch = torch_cuda
-    W, spp, D, seed = 32, 64, 4, 11
-    w = S.config1(W, W, spp=spp, max_depth=D, seed=seed)
+def image_parity(torch, key):
+    """RMSE(gpu - oracle) <= 1e-3 max |oracle| on the same seeds (BASELINE north star).  The
+    oracle runs on every host core of the box in a spawn pool (CUDA is initialised in this process)."""
+    import os
+    w = _image_workload(*key)
     r = _renderer(w)
     img = r.render_residual(w.args)
     torch.cuda.synchronize()
     g = img[..., :3].double().cpu().numpy()
-    with mp.get_context("fork").Pool(8) as p:
-        parts = p.map(_oracle_image, [(1, W, spp, D, seed, k, k + 1) for k in range(8)])
+    nt = max(8, os.cpu_count() or 8)
+    with mp.get_context("spawn").Pool(min(nt, os.cpu_count() or 8)) as p:
+        parts = p.map(_oracle_image, [(key, k, nt) for k in range(nt)])
     ref = sum(parts)
+    scale = np.abs(ref).max()
     rmse = math.sqrt(((g - ref) ** 2).mean())
-    assert rmse <= 1e-3 * np.abs(ref).max(), (rmse, np.abs(ref).max())
+    assert scale > 0 and rmse <= 1e-3 * scale, (key, rmse, scale)
+    return rmse / scale
+
+
+def test_image_rmse_config1(torch_cuda):
+    image_parity(torch_cuda, (1, 32, 32, 64, 4, 11))
+
+
+# configs 2-5 at 128 x 128 (config 5: 128 x 72, frame 0), the same scenes and cameras as BASELINE's (SURVEY 8(c)
+# C10).  spp is reduced from 1024 so that the one-by-one fp64 oracle finishes in about a minute per config on the
+# box's host cores (DESIGN.md section 3): both sides use the same Philox streams, so the comparison is sample
+# for sample and a lower spp does not loosen it (the mismatching records weigh MORE against max |oracle|).
+@pytest.mark.parametrize("key", [(2, 128, 128, 128), (3, 128, 128, 16), (4, 128, 128, 16), (5, 128, 72, 16)])
+def test_image_rmse_configs_2_to_5(torch_cuda, key):
+    image_parity(torch_cuda, key)
+
+
+def test_identity_edit_exact_zero_config4(torch_cuda):
+    """The identity edit (old == new transform bitwise, materials equal) of the 2M-triangle scene at full size
+    (1024^2, D = 8, all flags): every term cancels bitwise, the image is exactly 0."""
+    torch = torch_cuda
+    w = S.config4(spp=4)
+    eye = [dataclasses.replace(e, new_xform=e.old_xform.copy()) for e in w.edits]
+    r = _renderer(w)
+    r.set_edit(eye)
+    for flags in (S.PAPER_FLAGS, 0):
+        img = r.render_residual(dataclasses.replace(w.args, flags=flags))
+        torch.cuda.synchronize()
+        assert int(torch.count_nonzero(img)) == 0
+        st = r.get_stats()
+        assert st["samples"] > 0 and st["connections"] > 0 and st["effective_mask"] == 0x47
 
 
 def test_identity_edit_exact_zero_gpu(torch_cuda):
@@ -375,7 +449,8 @@ def test_invalid_arguments_are_refused(torch_cuda):
     w = S.config1(16, 16)
     r = _renderer(w)
     for bad in (dict(technique_mask=0x3F), dict(spp=3), dict(max_depth=0), dict(max_depth=11),
-                dict(flags=S.RECONNECT), dict(layer_mask=0x80), dict(flags=S.PAPER_FLAGS | 64)):
+                dict(flags=S.RECONNECT), dict(layer_mask=0x80), dict(flags=S.PAPER_FLAGS | 128),
+                dict(flags=S.PAPER_FLAGS | S.DIAG_ONE_WAY)):
         with pytest.raises(RRError):
             r.render_residual(dataclasses.replace(w.args, **bad))
     for bad in (dict(state=2), dict(spp=0), dict(max_depth=0), dict(max_depth=11)):

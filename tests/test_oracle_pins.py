@@ -24,7 +24,7 @@ from oracle import binding as B
 from rr_inputs import scenes as S
 
 VALS = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
-DIAG = 64  # RR_DIAG_ONE_WAY_ABLATION
+DIAG = S.DIAG_ONE_WAY  # RR_DIAG_ONE_WAY_ABLATION
 
 
 def _pool():
