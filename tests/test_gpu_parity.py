@@ -366,7 +366,9 @@ def image_parity(torch, key):
     ref = sum(parts)
     scale = np.abs(ref).max()
     rmse = math.sqrt(((g - ref) ** 2).mean())
-    assert scale > 0 and rmse <= 1e-3 * scale, (key, rmse, scale)
+    err = np.abs(g - ref).max(axis=2)
+    worst = np.unravel_index(np.argmax(err), err.shape)
+    assert scale > 0 and rmse <= 1e-3 * scale, (key, rmse, scale, "worst pixel", worst, float(err.max()))
     return rmse / scale
 
 
@@ -376,9 +378,9 @@ def test_image_rmse_config1(torch_cuda):
 
 # configs 2-5 at 128 x 128 (config 5: 128 x 72, frame 0), the same scenes and cameras as BASELINE's (SURVEY 8(c)
 # C10).  spp is reduced from 1024 so that the one-by-one fp64 oracle finishes in about a minute per config on the
-# box's host cores: both sides use the same Philox streams, so the comparison is sample
+# box's 16 host cores: both sides use the same Philox streams, so the comparison is sample
 # for sample and a lower spp does not loosen it (the mismatching records weigh MORE against max |oracle|).
-@pytest.mark.parametrize("key", [(2, 128, 128, 128), (3, 128, 128, 16), (4, 128, 128, 16), (5, 128, 72, 16)])
+@pytest.mark.parametrize("key", [(2, 128, 128, 256), (3, 128, 128, 64), (4, 128, 128, 64), (5, 128, 72, 64)])
 def test_image_rmse_configs_2_to_5(torch_cuda, key):
     image_parity(torch_cuda, key)
 
