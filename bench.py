@@ -125,29 +125,83 @@ def _oracle_worker(job):
     return time.perf_counter() - t, i1 - i0, st["closest_rays"] + st["shadow_rays"]
 
 
-def oracle_time(w, per_tech: int, cores: int):
-    """Time the oracle (as it stands) on the first `per_tech` indices of every (technique, side), split
-    over `cores` forked worker processes (counter-based RNG: disjoint index ranges are exact)."""
-    global _ORACLE, _ARGS
-    import multiprocessing as mp
-    from oracle import binding as OB
-    _ORACLE = OB.Oracle(w.scene, w.edits)
-    _ARGS = w.args
+ORACLE_PER_TECH = 4096   # indices per (technique, side) per timed sample (2^12)
+ORACLE_CHUNK = 256       # ... in chunks at seeded random positions over the whole index range
+ORACLE_PER_TECH_1CORE = 512
+
+
+def oracle_jobs(w, per_tech: int, seed: int = 0):
+    """(technique, side, i0, i1) chunks of about per_tech indices per (technique, side), spread over the WHOLE
+    index range (T7's pixel is i mod N_pix: every image row; the moved object at the image centre included)"""
     mask = _ORACLE.effective_mask(w.args.technique_mask)
+    n_all = _ORACLE.sample_range(w.args)
+    rng = np.random.default_rng(seed)
     jobs = []
-    chunk = max(1, per_tech // cores)
     for l in range(1, 8):
         if (mask >> (l - 1)) & 1:
-            for s in (0, 1):
-                for a in range(0, per_tech, chunk):
-                    jobs.append((l, s, a, min(per_tech, a + chunk)))
-    t0 = time.perf_counter()
-    with mp.get_context("fork").Pool(cores) as p:
-        res = p.map(_oracle_worker, jobs)
-    wall = time.perf_counter() - t0
-    n = sum(r[1] for r in res)
-    rays = sum(r[2] for r in res)
-    return n, rays, wall
+            for s in _ORACLE.sides(w.args):
+                k = max(1, per_tech // ORACLE_CHUNK)
+                starts = np.sort(rng.choice(max(1, n_all // ORACLE_CHUNK), size=k, replace=False)) * ORACLE_CHUNK
+                jobs += [(l, s, int(a), int(min(a + ORACLE_CHUNK, n_all))) for a in starts]
+    return jobs
+
+
+class OracleTimer:
+    """The oracle as it stands (single-threaded fp64 C++), on `cores` host processes.  The scene is loaded and
+    the fork pool started and warmed BEFORE the timer; the timed region is the pool's map over the jobs only
+    (counter-based RNG: disjoint index ranges are exact)."""
+
+    def __init__(self, w, cores: int):
+        global _ORACLE, _ARGS
+        import multiprocessing as mp
+        from oracle import binding as OB
+        _ORACLE = OB.Oracle(w.scene, w.edits)
+        _ARGS = w.args
+        self.w, self.cores = w, cores
+        self.pool = mp.get_context("fork").Pool(cores) if cores > 1 else None
+        if self.pool:
+            self.pool.map(_oracle_worker, [(7, 0, k, k + 1) for k in range(cores)])  # warm every worker
+
+    def time(self, per_tech: int, seed: int = 0):
+        jobs = oracle_jobs(self.w, per_tech, seed)
+        t0 = time.perf_counter()
+        res = self.pool.map(_oracle_worker, jobs, chunksize=1) if self.pool else [_oracle_worker(j) for j in jobs]
+        wall = time.perf_counter() - t0
+        return sum(r[1] for r in res), sum(r[2] for r in res), wall
+
+    def close(self):
+        if self.pool:
+            self.pool.close()
+            self.pool.join()
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(w, steps: int = 1):
+    """{1-core and all-core oracle samples/s on strided samples of the workload}"""
+    cores = cpu_cores()
+    one = OracleTimer(w, 1)
+    n1, _, t1 = one.time(ORACLE_PER_TECH_1CORE, seed=1)
+    allc = OracleTimer(w, cores)
+    n, rays, wall = 0, 0, 0.0
+    for k in range(steps):
+        a, b, c = allc.time(ORACLE_PER_TECH, seed=100 + k)
+        n, rays, wall = n + a, rays + b, wall + c
+    allc.close()
+    return {"value": n / wall, "unit": "samples/s", "cores": cores, "kind": "oracle",
+            "sample": f"{ORACLE_PER_TECH} indices of every (technique, side) in chunks of {ORACLE_CHUNK} at seeded "
+                      f"random positions over the whole index range of {w.name}, x{steps}",
+            "mrays_per_s": rays / wall / 1e6, "one_core_samples_per_s": n1 / t1,
+            "one_core_sample": f"{ORACLE_PER_TECH_1CORE} strided indices per (technique, side)",
+            "cpu_model": cpu_model(), "cpu_seconds": wall * cores}
 
 
 def cpu_cores() -> int:
@@ -163,13 +217,15 @@ def run_reference(a):
         return
     w = workload(a.config)
     cores = cpu_cores()
-    per_tech = 1024
+    per_tech = ORACLE_PER_TECH
     c = w.scene.camera
+    timer = OracleTimer(w, cores)
     vals = []
-    for k in range(a.warmup + a.steps):
-        n, rays, wall = oracle_time(w, per_tech, cores)
+    for k in range(a.warmup + a.steps):  # each step: a fresh strided sample of the workload
+        n, rays, wall = timer.time(per_tech, seed=100 + k)
         if k >= a.warmup:
             vals.append((n, rays, wall))
+    timer.close()
     n = sum(v[0] for v in vals)
     wall = sum(v[2] for v in vals)
     rays = sum(v[1] for v in vals)
@@ -179,10 +235,13 @@ def run_reference(a):
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * wall / max(1, a.steps),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "scene": w.scene.name, "resolution": [c.width, c.height], "spp": w.args.spp,
-                   "max_depth": w.args.max_depth, "sample": f"first {per_tech} indices of each (technique, side) per step"},
+                   "max_depth": w.args.max_depth,
+                   "sample": f"{per_tech} strided indices of each (technique, side) per step (chunks of {ORACLE_CHUNK})"},
         "mrays_per_s": rays / wall / 1e6,
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "oracle",
-                         "sample": f"first {per_tech} indices of each (technique, side), {a.steps} timed steps"},
+                         "sample": f"{per_tech} indices of each (technique, side) in chunks of {ORACLE_CHUNK} at seeded "
+                                   f"random positions over the whole index range, {a.steps} timed steps",
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -205,6 +264,11 @@ def run_ours(a):
     w = workload(a.config)
     args = w.args
     c = w.scene.camera
+    # CPU baseline (the oracle on the host cores) first, rank 0 at N = 1 only: before this process touches CUDA,
+    # so the oracle's fork pool never forks a CUDA context
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(w)
     r = Renderer(local)
     t0 = time.time()
     r.upload(w.scene)
@@ -347,15 +411,6 @@ def run_ours(a):
     d2h = int(host.nbytes) * (2 if world > 1 and rank == 0 else 1)
     e2e = {"value": total_samples * a.e2e_steps / float(el.item()), "unit": "samples/s",
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
-    # ---- CPU baseline (oracle) on the host cores, rank 0 at N = 1 only
-    cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cores = cpu_cores()
-        per_tech = 256
-        n, rays, wall = oracle_time(w, per_tech, cores)
-        cpu = {"value": n / wall, "unit": "samples/s", "cores": cores, "kind": "oracle",
-               "sample": f"first {per_tech} indices of each (technique, side) of {w.name}",
-               "mrays_per_s": rays / wall / 1e6}
     if rank == 0:
         line = {
             "metric": "residual_samples_per_s", "value": value, "unit": "samples/s", "n_gpus": world,
