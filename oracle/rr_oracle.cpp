@@ -367,9 +367,18 @@ bool visible(const Scene& S, int F, V3 a, V3 b, int excl_a, int excl_b, Counters
   return !blocked;
 }
 
+// The ghost point x_G a T4 / T5 / T6 sample passed its edge through (reading 12): the edge crosses
+// the ghost there by construction, so that crossing is a candidate whether or not a ray query finds it.
+struct SeedCrossing {
+  int edge = -1;  // path edge (i, i+1) through x_G; -1: none
+  V3 p, n;        // x_G and the ghost's normal there
+};
+
 // ghost crossings of segment (a,b) in state F: hits of moved objects placed at M_Fbar in
-// (eps, len - eps), sorted by t, hits within 1e-6 diag merged
-std::vector<Crossing> crossings(const Scene& S, int F, V3 a, V3 b) {
+// (eps, len - eps), sorted by t, hits within 1e-6 diag merged.  seed: a crossing known to
+// lie on the segment (x_G of the sample that produced it); a hit within the merge distance of it is the
+// same crossing.
+std::vector<Crossing> crossings(const Scene& S, int F, V3 a, V3 b, const SeedCrossing* seed = nullptr) {
   std::vector<Crossing> out;
   V3 dv = b - a;
   double L = len(dv);
@@ -384,7 +393,19 @@ std::vector<Crossing> crossings(const Scene& S, int F, V3 a, V3 b) {
   std::sort(hits.begin(), hits.end(), [](const std::pair<double, const Tri*>& x,
                                          const std::pair<double, const Tri*>& y) { return x.first < y.first; });
   double tol = 1e-6 * S.diag;
+  double ts = seed ? dot(seed->p - a, d) : 0.0;
+  bool seeded = false;
+  auto put_seed = [&]() {
+    Crossing c;
+    c.t = ts;
+    c.p = seed->p;
+    c.n = seed->n;
+    out.push_back(c);
+    seeded = true;
+  };
   for (auto& h : hits) {
+    if (seed && std::fabs(h.first - ts) < tol) continue;  // the known crossing itself
+    if (seed && !seeded && h.first > ts) put_seed();
     if (!out.empty() && h.first - out.back().t < tol) continue;
     Crossing c;
     c.t = h.first;
@@ -392,6 +413,7 @@ std::vector<Crossing> crossings(const Scene& S, int F, V3 a, V3 b) {
     c.n = h.second->n;
     out.push_back(c);
   }
+  if (seed && !seeded) put_seed();
   return out;
 }
 
@@ -671,7 +693,7 @@ struct Ctx {
   std::vector<double>* recon_out = nullptr;  // test export: geometry of accepted reconnections (orc_reconnections)
 };
 
-Eval eval_path(Ctx& cx, int F, const Path& P, bool check_walk_vis = true) {
+Eval eval_path(Ctx& cx, int F, const Path& P, bool check_walk_vis = true, const SeedCrossing* seed = nullptr) {
   const Scene& S = *cx.S;
   Eval ev;
   const std::vector<Vtx>& x = P.x;
@@ -682,7 +704,7 @@ Eval eval_path(Ctx& cx, int F, const Path& P, bool check_walk_vis = true) {
   ev.cross.resize(k - 1);
   for (int e = 0; e < k - 1; ++e) {
     if (check_walk_vis) ev.edge_vis[e] = visible(S, F, x[e].p, x[e + 1].p, x[e].tri, x[e + 1].tri, &cx.C) ? 1 : 0;
-    ev.cross[e] = crossings(S, F, x[e].p, x[e + 1].p);
+    ev.cross[e] = crossings(S, F, x[e].p, x[e + 1].p, (seed && seed->edge == e) ? seed : nullptr);
   }
   // ---- f (Eq.2)
   V3 f = v3(1, 1, 1);
@@ -1020,6 +1042,17 @@ struct Conn {
   int prod_tech = 0, prod_elem = 0;  // the producing candidate: technique and vertex / edge index
 };
 
+// The producing ghost crossing of a connection path of a T4 / T5 / T6 sample (none for the other techniques)
+SeedCrossing seed_of(const Gen& g, const Conn& c) {
+  SeedCrossing sd;
+  if (g.tech < 4 || g.tech > 6) return sd;
+  int k = (int)c.path.x.size();
+  sd.edge = g.tech == 5 ? 0 : (g.tech == 4 ? k - 2 : c.prod_elem);
+  sd.p = g.start.p;
+  sd.n = g.start.n;
+  return sd;
+}
+
 // Build every connection path of a generated sample (in its own state)
 std::vector<Conn> connections(Ctx& cx, const Gen& g, const Stream& st, int D) {
   const Scene& S = *cx.S;
@@ -1349,7 +1382,8 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
     r.pix_p = c.path.pixel;
     r.pix_q = -1;
     r.R = 1.0;
-    Eval ep = eval_path(cx, F, c.path);
+    const SeedCrossing sp = seed_of(gp, c);
+    Eval ep = eval_path(cx, F, c.path, true, &sp);
     double vp[3];
     value(ep, vp);
     offscreen_zero(c, c.path.pixel, vp);
@@ -1389,7 +1423,13 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
             for (int m = (int)walk_q.size() - 1; m >= 0; --m) q.x.push_back(walk_q[m]);
             q.x.push_back(c.path.x.back());
           }
-          eq = eval_path(cx, Fb, q);
+          SeedCrossing sq;  // the mapped T4 / T5's x_G' on q's first / last edge (reconnection: single walks only)
+          if (gq.tech == 4 || gq.tech == 5) {
+            sq.edge = gq.tech == 5 ? 0 : (int)q.x.size() - 2;
+            sq.p = gq.start.p;
+            sq.n = gq.start.n;
+          }
+          eq = eval_path(cx, Fb, q, true, &sq);
           // walk edges of q from the reconnection on must be unoccluded in View_Fbar
           int k = (int)q.x.size();
           for (int e = 0; e < k - 1; ++e) {
@@ -1423,7 +1463,8 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
       }
     } else if (cq_match) {
       q = cq_match->path;
-      eq = eval_path(cx, Fb, q);
+      const SeedCrossing sq = seed_of(gq, *cq_match);
+      eq = eval_path(cx, Fb, q, true, &sq);
       have_q = true;
     } else {
       status = ST_UNPAIRED;
@@ -1487,7 +1528,8 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
       for (const Conn* u : used_q)
         if (u == &c) used = true;
       if (used) continue;
-      Eval eq = eval_path(cx, Fb, c.path);
+      const SeedCrossing sq = seed_of(gq, c);
+      Eval eq = eval_path(cx, Fb, c.path, true, &sq);
       double vq[3];
       value(eq, vq);
       offscreen_zero(c, c.path.pixel, vq);

@@ -368,6 +368,7 @@ __device__ __forceinline__ Cross cross_zero() { Cross c; c.n = c.s0 = c.sa = c.s
 
 struct QCount {  // per-thread query counters
   uint32_t closest, shadow, inst;
+  uint32_t seen_overflow;  // ghost crossings beyond RR_SEEN per (query, state): not deduplicated (rr_stats.sched[6])
   TCount tc;
 };
 

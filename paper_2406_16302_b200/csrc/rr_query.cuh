@@ -20,6 +20,9 @@
 namespace rr {
 
 enum { QT_CLOSEST = 0, QT_SEG = 1 };
+#ifndef RR_SEEN
+#define RR_SEEN 16  // ghost-crossing distances remembered per (query, state) for the shared-edge dedup
+#endif
 
 
 
@@ -33,6 +36,10 @@ struct __align__(16) Query {
   int ea, eb;            // excluded triangles (origin, end)
   uint8_t type, want;    // want: bit F set -> evaluate state F
   uint8_t dyn_only, pad;
+  // the ghost point x_G a T4 / T5 / T6 sample sent this ray / segment through (reading 12): a crossing
+  // at distance seed_t (> 0) with 1/|cos| = seed_ic that counts whether or not the (non-watertight) triangle test
+  // finds it; found hits within dedup_tol of it are the same crossing.  seed_t = 0: none.
+  float seed_t, seed_ic;
 };
 
 struct __align__(16) QRes {
@@ -147,8 +154,14 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
   best_t[0] = best_t[1] = thi;
   bool blocked[2] = {false, false};
   bool sblock = false;
-  float seen[8];
+  float seen[RR_SEEN];
   int ns = 0, seen_state = -1;
+  if (q.seed_t > 0.0f) {  // the sample's own crossing (single-state query); its (L - t) term is added at the end
+    const int G = (q.want & 1) ? 0 : 1;
+    r.c[G].n = 1.0f;
+    r.c[G].s0 = q.seed_ic;
+    r.c[G].sa = q.seed_t * q.seed_t * q.seed_ic;
+  }
   const int NI = S.n_inst;
   const int njobs = 1 + 4 * NI;
   for (int j = 0; j < njobs; ++j) {
@@ -187,6 +200,7 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
         if (seen_state != F) {
           ns = 0;
           seen_state = F;
+          if (q.seed_t > 0.0f) seen[ns++] = q.seed_t;
         }
       }
     }
@@ -194,9 +208,11 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
     WRay wr = make_wray(o, d);
     traverse<COUNT>(S, root, wr, tmin, tmax, [&](int li, float t, float tm, int id) -> float {
       if (kind == 2) {  // ghost crossing (all hits, dedup within dedup_tol)
-        for (int a = 0; a < ns; ++a)
+        for (int a = 0; a < min(ns, RR_SEEN); ++a)
           if (fabsf(seen[a] - t) < S.dedup_tol) return tm;
-        if (ns < 8) seen[ns++] = t;
+        if (ns < RR_SEEN) seen[ns] = t;
+        else qc.seen_overflow++;  // beyond RR_SEEN crossings: counted, no longer deduplicated (rr_stats.sched[6])
+        ns++;
         const float4* tp = S.ltris + 3 * li;
         float4 a4 = __ldg(tp), b4 = __ldg(tp + 1), c4 = __ldg(tp + 2);
         float3 nrm = norm3_exact(cross3(f3(b4.x - a4.x, b4.y - a4.y, b4.z - a4.z), f3(c4.x - a4.x, c4.y - a4.y, c4.z - a4.z)));
@@ -225,6 +241,11 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
       return t;
     }, qc.tc);
   }
+  if (q.seed_t > 0.0f) {
+    const int G = (q.want & 1) ? 0 : 1;
+    const float Lc = seg ? L : best_t[G];
+    r.c[G].sb += (Lc - q.seed_t) * (Lc - q.seed_t) * q.seed_ic;
+  }
   for (int F = 0; F < 2; ++F) {
     if (!((q.want >> F) & 1)) continue;
     if (seg) {
@@ -248,6 +269,7 @@ __device__ __forceinline__ Query mk_ray(P3 o, float3 d, int excl, int want) {
   q.type = QT_CLOSEST;
   q.want = (uint8_t)want;
   q.dyn_only = 0;
+  q.seed_t = q.seed_ic = 0.0f;
   return q;
 }
 __device__ __forceinline__ Query mk_seg(P3 a, P3 b, int ea, int eb, int want, bool dyn_only = false) {
@@ -262,6 +284,7 @@ __device__ __forceinline__ Query mk_seg(P3 a, P3 b, int ea, int eb, int want, bo
   q.type = QT_SEG;
   q.want = (uint8_t)want;
   q.dyn_only = dyn_only ? 1 : 0;
+  q.seed_t = q.seed_ic = 0.0f;
   return q;
 }
 

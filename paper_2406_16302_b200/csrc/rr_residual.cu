@@ -83,6 +83,12 @@ struct SState {
 };
 
 __device__ __forceinline__ bool nee_ok(int tech, int m) { return tech == 2 ? m >= 2 : true; }
+// the sample's own ghost crossing on the queried edge (Query::seed_t; reading 12)
+__device__ __forceinline__ Query seeded(Query q, float t, float3 nG) {
+  q.seed_t = t;
+  q.seed_ic = 1.0f / fabsf(dot3(nG, q.d));
+  return q;
+}
 
 // issue the start query of one side
 __device__ void start_issue(const DevScene& S, int tech, int F, const float d0[8], SStart& s, Batch& B) {
@@ -114,7 +120,7 @@ __device__ void start_issue(const DevScene& S, int tech, int F, const float d0[8
       if (!(s.dl > S.eps)) return;
       s.dir = dv * (1.0f / s.dl);
       if (!(dot3(s.a.n, s.dir) > 0.0f)) return;
-      s.qi = B.push(mk_ray(s.a.p, s.dir, s.a.tri, bit(F)));
+      s.qi = B.push(seeded(mk_ray(s.a.p, s.dir, s.a.tri, bit(F)), s.dl, xg.n));
       return;
     }
     case 5: {  // ghost from sensor
@@ -125,7 +131,7 @@ __device__ void start_issue(const DevScene& S, int tech, int F, const float d0[8
       float3 dv = sub3(xg.p, E.p);
       s.dl = sqrtf(dot3(dv, dv));
       s.dir = dv * (1.0f / s.dl);
-      s.qi = B.push(mk_ray(E.p, s.dir, -1, bit(F)));
+      s.qi = B.push(seeded(mk_ray(E.p, s.dir, -1, bit(F)), s.dl, xg.n));
       return;
     }
   }
@@ -577,8 +583,11 @@ __device__ void bidir_issue(const DevScene& S, const KArgs& A, int tech, int F, 
   G.qyz = -1;
   G.A.qw = G.B.qw = G.A.qc = G.B.qc = -1;
   if (!G.ok) return;
-  if (first && tech == 6 && S.n_moved > 0) {
-    G.qyz = B.push(mk_seg(G.A.v[0].p, G.A.v[1].p, -2, -2, bit(F)));  // crossings of the whole edge
+  if (first && tech == 6 && S.n_moved > 0) {  // crossings of the whole edge y_1 -> z_1, x_G among them
+    Query q = mk_seg(G.A.v[0].p, G.A.v[1].p, -2, -2, bit(F));
+    const P3 a = G.A.v[0].p;
+    const double gx = G.start.p.x - a.x, gy = G.start.p.y - a.y, gz = G.start.p.z - a.z;
+    G.qyz = B.push(seeded(q, (float)sqrt(gx * gx + gy * gy + gz * gz), G.start.n));
   }
   PV E = cam_pv(S);
   for (int side = 0; side < 2; ++side) {
@@ -803,7 +812,7 @@ template <class State, bool BIDIR, bool COUNT>
 __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A) {
   Out o;
   o.A = &A;
-  o.qc.closest = o.qc.shadow = o.qc.inst = 0;
+  o.qc.closest = o.qc.shadow = o.qc.inst = o.qc.seen_overflow = 0;
   o.qc.tc.nodes = o.qc.tc.tris = 0;
   o.conns = o.acc = o.rej = o.unp = o.monly = o.recon = o.splats = o.offscreen = o.zero = 0;
   for (int r = 0; r < 6; ++r) o.rejby[r] = 0;
@@ -891,6 +900,7 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
   for (int r = 0; r < 6; ++r) warp_add(stt + STAT_REJBY + r, o.rejby[r]);
   for (int r = 0; r < 5; ++r)
     if (sc[r]) atomicAdd(stt + STAT_SCHED + r, sc[r]);
+  warp_add(stt + STAT_SCHED + 6, o.qc.seen_overflow);
 }
 
 template <bool COUNT>
