@@ -101,6 +101,14 @@ enum {
   RR_VNDF = 32u,           /* sample GGX directions from the visible normals of the incoming direction (Heitz
                               2018) instead of D(h)|n.h|; pdfs and MIS follow.  A variance-only variant
                               (SURVEY 8(f) row 4); residual renders only (the primal renderer ignores it) */
+  RR_PRIMAL_SHARED_STREAMS = 128u, /* rr_render_primal only: the same random numbers for both states (Philox stream
+                              state 0), so that primal(new) - primal(old) is a correlated, unbiased estimate of the
+                              residual (the quality harness's reference, independent of the residual estimator) */
+  RR_NO_PATH_MAPPING = 256u, /* "incremental w/o PM" (Table num_of_dynamics): both states
+                              sampled by every technique (RR_TWO_WAY required, RR_RECONNECT / RR_REJECT_MULTI off),
+                              no mapped path -- each base connection splats 2 sigma_F v_F(p) / spp, and a path with
+                              no vertex on an edited object and no ghost crossing in its own state (a static path,
+                              equal in both states) is rejected.  Unbiased; the ablation of path mapping */
   RR_DIAG_ONE_WAY_ABLATION = 64u /* DIAGNOSTIC, deliberately biased: one-way
                               (side N only, N_pix*spp samples per technique, RR_TWO_WAY must be off) but with the
                               two-way pairing rules (RR_RECONNECT / RR_REJECT_MULTI allowed); accepted pairs splat
@@ -118,7 +126,8 @@ typedef struct {
   uint32_t technique_mask; /* bit l-1 enables technique l (T1..T7); must contain T7 (bit 6) */
   uint32_t flags;          /* RR_* flags above; RR_PAPER_FLAGS = the paper's method; mask 0x40 + flags 0 =
                               correlated PT.  RR_RECONNECT / RR_REJECT_MULTI need RR_TWO_WAY or
-                              RR_DIAG_ONE_WAY_ABLATION; the latter excludes RR_TWO_WAY (RR_E_INVALID otherwise) */
+                              RR_DIAG_ONE_WAY_ABLATION; the latter excludes RR_TWO_WAY; RR_NO_PATH_MAPPING needs
+                              RR_TWO_WAY alone (RR_E_INVALID otherwise) */
   float jacobian_max;      /* 10 */
   float alpha_min;         /* roughness threshold, 0.1 */
   float dmin_rel;          /* distance threshold / scene diagonal, 0.01 */
@@ -145,7 +154,7 @@ typedef struct {
                               rounds, [2] sample steps, [3] queries per round summed, [4] lanes holding
                               a sample summed over rounds, [5] deepest BVH root-to-leaf path in inner
                               nodes (scene property; upload fails above RR_STACK = 64), [6] ghost
-                              crossings beyond the 16 remembered per (query, state) for the shared-edge dedup
+                              crossings beyond the 8 remembered per (query, state) for the shared-edge dedup
                               (counted, not deduplicated; 0 on the BASELINE scenes), ([1], [7] reserved, 0) */
 } rr_stats;
 
@@ -196,8 +205,8 @@ rr_status rr_render_residual_host(rr_ctx* ctx, const rr_render_args* args, float
 /* Primal image I^D(state) (Eq.1-2; state 0 = new, 1 = old) by unidirectional path
  * tracing with next-event estimation and BSDF sampling combined by the balance heuristic, spp samples per
  * pixel, paths of <= max_depth edges, Philox key `seed` (streams disjoint from the residual ones).  Writes
- * (overwrites) d_image_rgba (H*W*4 fp32, device, channel 3 = 0); RR_COUNT_TRAVERSAL in `flags` counts node
- * fetches into rr_stats.  The image a residual is added to: I_new = I_old + residual.
+ * (overwrites) d_image_rgba (H*W*4 fp32, device, channel 3 = 0); `flags`: RR_COUNT_TRAVERSAL counts node
+ * fetches into rr_stats, RR_PRIMAL_SHARED_STREAMS uses one stream for both states (other bits: RR_E_INVALID).  The image a residual is added to: I_new = I_old + residual.
  * Asynchronous on cuda_stream.  Errors: RR_E_INVALID (null image, spp = 0, max_depth out of 1..RR_MAX_DEPTH,
  * state > 1), RR_E_STATE (before upload), RR_E_CUDA. */
 rr_status rr_render_primal(rr_ctx* ctx, uint32_t state, uint32_t spp, uint64_t seed, uint32_t max_depth,

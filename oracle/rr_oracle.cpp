@@ -372,12 +372,13 @@ bool visible(const Scene& S, int F, V3 a, V3 b, int excl_a, int excl_b, Counters
 struct SeedCrossing {
   int edge = -1;  // path edge (i, i+1) through x_G; -1: none
   V3 p, n;        // x_G and the ghost's normal there
+  int tri = -1;   // the ghost triangle x_G was sampled on
 };
 
 // ghost crossings of segment (a,b) in state F: hits of moved objects placed at M_Fbar in
 // (eps, len - eps), sorted by t, hits within 1e-6 diag merged.  seed: a crossing known to
 // lie on the segment (x_G of the sample that produced it); a hit within the merge distance of it is the
-// same crossing.
+// same crossing, and so is a hit of the seed's own triangle (a segment crosses a plane once).
 std::vector<Crossing> crossings(const Scene& S, int F, V3 a, V3 b, const SeedCrossing* seed = nullptr) {
   std::vector<Crossing> out;
   V3 dv = b - a;
@@ -404,7 +405,7 @@ std::vector<Crossing> crossings(const Scene& S, int F, V3 a, V3 b, const SeedCro
     seeded = true;
   };
   for (auto& h : hits) {
-    if (seed && std::fabs(h.first - ts) < tol) continue;  // the known crossing itself
+    if (seed && (std::fabs(h.first - ts) < tol || h.second->id == seed->tri)) continue;  // the known crossing itself
     if (seed && !seeded && h.first > ts) put_seed();
     if (!out.empty() && h.first - out.back().t < tol) continue;
     Crossing c;
@@ -629,6 +630,7 @@ struct Eval {
   bool walk_edge_blocked = false;
   std::vector<int> edge_vis;
   std::vector<std::vector<Crossing>> cross;
+  bool dynamic = false;         // some vertex on an edited object or some edge crossing a ghost
   std::vector<Cand> cands;      // the candidates of Pi, in order, and each one's technique pdf (C5 table)
   std::vector<double> cand_p;
 };
@@ -734,6 +736,7 @@ Eval eval_path(Ctx& cx, int F, const Path& P, bool check_walk_vis = true, const 
   std::vector<int> dyn(k, 0), nc(k - 1, 0);
   for (int i = 1; i <= k - 2; ++i) dyn[i] = (x[i].kind == K_SURF && S.edited[x[i].obj]) ? 1 : 0;
   for (int e = 0; e < k - 1; ++e) nc[e] = (int)ev.cross[e].size();
+  for (int i = 0; i < k; ++i) ev.dynamic = ev.dynamic || dyn[i] || (i < k - 1 && nc[i] > 0);
   std::vector<Cand> cands = enumerate_candidates(k, dyn, nc, cx.mask);
   ev.n_cand = (int)cands.size();
   double pA_D = S.edited_set.area > 0 ? 1.0 / S.edited_set.area : 0.0;
@@ -1050,6 +1053,7 @@ SeedCrossing seed_of(const Gen& g, const Conn& c) {
   sd.edge = g.tech == 5 ? 0 : (g.tech == 4 ? k - 2 : c.prod_elem);
   sd.p = g.start.p;
   sd.n = g.start.n;
+  sd.tri = g.start.tri;
   return sd;
 }
 
@@ -1219,7 +1223,8 @@ typedef struct {
   uint32_t max_depth;
   uint32_t technique_mask;
   uint32_t flags;  // 1 TWO_WAY, 2 RECONNECT, 4 REJECT_MULTI, 32 VNDF (GGX visible-normal sampling),
-                   // 64 DIAG_ONE_WAY_ABLATION (one-way with the two-way pairing rules; deliberately biased)
+                   // 64 DIAG_ONE_WAY_ABLATION (one-way with the two-way pairing rules; deliberately biased),
+                   // 256 NO_PATH_MAPPING (two-way sampling, no mapped paths, static paths rejected)
   double jacobian_max, alpha_min, dmin_rel;
 } orc_args;
 
@@ -1280,6 +1285,11 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
   // weight 1 and paths of O that no N sample maps to are never counted.  It is the estimator P:L425 warns
   // about ("two-way path mapping to ensure the coverage"): biased by construction, a test mode only.
   const bool diag = (A.flags & 64) != 0 && !(A.flags & 1);
+  // "Incremental w/o PM" (Table num_of_dynamics): both frames rendered separately with
+  // the dynamic sampling techniques, no path mapping.  Every base connection is unpaired (weight 2 per side) and
+  // a path with no dynamic vertex and no ghost crossing in its own state (a static path, equal f and Pi in both
+  // states) is rejected outright: those cancel between the two states in expectation.
+  const bool nopm = (A.flags & 256) != 0 && (A.flags & 1);
   const bool two_way = A.flags & 1, paired = two_way || diag;
   const bool reconnect = (A.flags & 2) && paired, reject_multi = (A.flags & 4) && paired;
   const double spp = (double)A.spp;
@@ -1287,7 +1297,7 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
   int lq = paired_tech(S, cx.mask, l);
 
   Gen gp = generate(cx, l, F, st, D);
-  Gen gq = generate(cx, lq, Fb, st, D);  // random-seed replay: same counters
+  Gen gq = nopm ? Gen() : generate(cx, lq, Fb, st, D);  // random-seed replay: same counters
   std::vector<Conn> cp = connections(cx, gp, st, D);
   std::vector<Conn> cq = connections(cx, gq, st, D);
   if (stats) stats->samples++;
@@ -1387,6 +1397,7 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
     double vp[3];
     value(ep, vp);
     offscreen_zero(c, c.path.pixel, vp);
+    if (nopm && !ep.dynamic) vp[0] = vp[1] = vp[2] = 0.0;
     r.n_cand_p = ep.n_cand;
     for (int ch = 0; ch < 3; ++ch) r.v_p[ch] = vp[ch];
 
@@ -1428,6 +1439,7 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
             sq.edge = gq.tech == 5 ? 0 : (int)q.x.size() - 2;
             sq.p = gq.start.p;
             sq.n = gq.start.n;
+            sq.tri = gq.start.tri;
           }
           eq = eval_path(cx, Fb, q, true, &sq);
           // walk edges of q from the reconnection on must be unoccluded in View_Fbar

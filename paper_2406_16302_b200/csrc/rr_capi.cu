@@ -684,8 +684,11 @@ static rr_status check_args(rr_ctx* c, const rr_render_args* a) {
     return fail(c, RR_E_INVALID, "RR_RECONNECT / RR_REJECT_MULTI require RR_TWO_WAY (or RR_DIAG_ONE_WAY_ABLATION)");
   if ((a->flags & RR_TWO_WAY) && (a->flags & RR_DIAG_ONE_WAY_ABLATION))
     return fail(c, RR_E_INVALID, "RR_DIAG_ONE_WAY_ABLATION is one-way: RR_TWO_WAY must be off");
+  if ((a->flags & RR_NO_PATH_MAPPING) &&
+      (!(a->flags & RR_TWO_WAY) || (a->flags & (RR_RECONNECT | RR_REJECT_MULTI | RR_DIAG_ONE_WAY_ABLATION))))
+    return fail(c, RR_E_INVALID, "RR_NO_PATH_MAPPING needs RR_TWO_WAY without RR_RECONNECT / RR_REJECT_MULTI");
   if (a->flags & ~(RR_TWO_WAY | RR_RECONNECT | RR_REJECT_MULTI | RR_ACCUMULATE | RR_COUNT_TRAVERSAL | RR_VNDF |
-                   RR_DIAG_ONE_WAY_ABLATION))
+                   RR_DIAG_ONE_WAY_ABLATION | RR_NO_PATH_MAPPING))
     return fail(c, RR_E_INVALID, "unknown flag bits");
   if (a->shard_count == 0 || a->shard_index >= a->shard_count) return fail(c, RR_E_INVALID, "bad shard");
   return RR_OK;
@@ -714,6 +717,8 @@ static KArgs make_kargs(rr_ctx* c, const rr_render_args* a, uint32_t mask, int l
   // the diagnostic one-way ablation; the ablation changes the weights only (rr_shade.cuh finish)
   K.two_way = (a->flags & (RR_TWO_WAY | RR_DIAG_ONE_WAY_ABLATION)) ? 1 : 0;
   K.diag = (a->flags & RR_DIAG_ONE_WAY_ABLATION) ? 1 : 0;
+  K.nopm = (a->flags & RR_NO_PATH_MAPPING) ? 1 : 0;
+  if (K.nopm) K.mask |= 0x100u;  // path_value: static paths rejected
   K.count = (a->flags & RR_COUNT_TRAVERSAL) ? 1 : 0;
   K.mat_type_vndf = (a->flags & RR_VNDF) ? c->mat_type_vndf.p : nullptr;
   K.reconnect = (a->flags & RR_RECONNECT) ? 1 : 0;
@@ -786,7 +791,9 @@ rr_status rr_render_primal(rr_ctx* c, uint32_t state, uint32_t spp, uint64_t see
   cudaStream_t st = (cudaStream_t)stream;
   cudaMemsetAsync(d_image, 0, (size_t)c->cam.width * c->cam.height * 4 * sizeof(float), st);
   cudaMemsetAsync(c->stats.p, 0, STAT_COUNT * sizeof(unsigned long long), st);
-  launch_primal(c->S, (int)state, seed, (int)max_depth, spp, d_image, c->stats.p, (flags & RR_COUNT_TRAVERSAL) != 0, st);
+  if (flags & ~(uint32_t)(RR_COUNT_TRAVERSAL | RR_PRIMAL_SHARED_STREAMS)) return fail(c, RR_E_INVALID, "unknown primal flag bits");
+  launch_primal(c->S, (int)state, seed, (int)max_depth, spp, d_image, c->stats.p, (flags & RR_COUNT_TRAVERSAL) != 0,
+                (flags & RR_PRIMAL_SHARED_STREAMS) != 0, st);
   return cuda_check(c, "primal launch");
 }
 

@@ -19,6 +19,7 @@ struct KArgs {
   uint32_t mask;
   int two_way, reconnect, reject_multi;  // two_way: paired control flow (RR_TWO_WAY or the diagnostic ablation)
   int diag;                              // RR_DIAG_ONE_WAY_ABLATION weights
+  int nopm;                              // RR_NO_PATH_MAPPING: no mapped path (mask bit 8: static paths rejected)
   uint64_t seed;
   float sigma, inv_spp, jacobian_max, alpha_min, dmin;
   uint64_t n_total;                  // samples of this (technique, side) over all shards
@@ -41,7 +42,7 @@ void launch_residual_vndf(const DevScene& S, const KArgs& A, int grid, cudaStrea
 int residual_grid(bool bidir, uint64_t n);  // blocks of residual_block() threads for n sample slots
 int residual_block();
 void launch_primal(const DevScene& S, int F, uint64_t seed, int D, uint32_t spp, float* image,
-                   unsigned long long* stats, bool count, cudaStream_t st);
+                   unsigned long long* stats, bool count, bool shared_streams, cudaStream_t st);
 void launch_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out, cudaStream_t st);
 void launch_trace(const DevScene& S, int F, uint32_t n, const float* rays, float* hits, cudaStream_t st);
 void launch_segment(const DevScene& S, uint32_t n, const float* segs, float* out, cudaStream_t st);

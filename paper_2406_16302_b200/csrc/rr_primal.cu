@@ -2,8 +2,11 @@
 //
 // Unidirectional path tracing of the primal path integral (Eq.1-2) in state F, paths
 // of at most D edges, with next-event estimation and BSDF sampling combined by the balance heuristic in
-// solid angle.  Random numbers: Philox counter (sample index lo/hi, 0x80 | F << 8, 2 slot + call), key =
-// seed -- technique id 0x80 is never used by the residual streams.  Composite: I_new = I_old + residual.
+// solid angle.  Random numbers: Philox counter (sample index lo/hi, 0x80 | stream_state << 8, 2 slot + call),
+// key = seed -- technique id 0x80 is never used by the residual streams; stream_state = F, or 0 for both states
+// (RR_PRIMAL_SHARED_STREAMS: the two images then use the same random numbers and their difference is a
+// correlated, unbiased estimate of I(N) - I(O), the quality harness's reference).  Composite: I_new = I_old +
+// residual.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -27,7 +30,7 @@ __device__ __forceinline__ bool nonzero3(float3 v) { return v.x != 0.0f || v.y !
 template <bool COUNT>
 __global__ void __launch_bounds__(RR_PRIMAL_BLOCK, 8) k_primal(const __grid_constant__ DevScene S, int F, uint64_t seed,
                                                               int D, uint64_t n, float inv_spp, float* image,
-                                                              unsigned long long* stats) {
+                                                              unsigned long long* stats, int stream_state) {
   QCount qc = {};
   const int npix = S.W * S.H;
   const PV E = cam_pv(S);
@@ -35,7 +38,7 @@ __global__ void __launch_bounds__(RR_PRIMAL_BLOCK, 8) k_primal(const __grid_cons
     Rng rng;
     rng.i_lo = (uint32_t)idx;
     rng.i_hi = (uint32_t)(idx >> 32);
-    rng.ls = 0x80u | ((uint32_t)F << 8);
+    rng.ls = 0x80u | ((uint32_t)stream_state << 8);
     rng.k0 = (uint32_t)seed;
     rng.k1 = (uint32_t)(seed >> 32);
     const int pix = (int)(idx % (uint64_t)npix);
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(RR_PRIMAL_BLOCK, 8) k_primal(const __grid_cons
 }
 
 void launch_primal(const DevScene& S, int F, uint64_t seed, int D, uint32_t spp, float* image,
-                   unsigned long long* stats, bool count, cudaStream_t st) {
+                   unsigned long long* stats, bool count, bool shared_streams, cudaStream_t st) {
   static int grid = 0;
   if (!grid) {
     int dev = 0, sms = 148, occ = 1;
@@ -124,8 +127,9 @@ void launch_primal(const DevScene& S, int F, uint64_t seed, int D, uint32_t spp,
   }
   uint64_t n = (uint64_t)S.W * S.H * spp;
   int g = (int)std::min<uint64_t>((uint64_t)grid, (n + RR_PRIMAL_BLOCK - 1) / RR_PRIMAL_BLOCK);
-  if (count) k_primal<true><<<g, RR_PRIMAL_BLOCK, 0, st>>>(S, F, seed, D, n, 1.0f / (float)spp, image, stats);
-  else k_primal<false><<<g, RR_PRIMAL_BLOCK, 0, st>>>(S, F, seed, D, n, 1.0f / (float)spp, image, stats);
+  const int ss = shared_streams ? 0 : F;
+  if (count) k_primal<true><<<g, RR_PRIMAL_BLOCK, 0, st>>>(S, F, seed, D, n, 1.0f / (float)spp, image, stats, ss);
+  else k_primal<false><<<g, RR_PRIMAL_BLOCK, 0, st>>>(S, F, seed, D, n, 1.0f / (float)spp, image, stats, ss);
 }
 
 }  // namespace rr

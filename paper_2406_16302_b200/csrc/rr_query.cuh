@@ -21,7 +21,7 @@ namespace rr {
 
 enum { QT_CLOSEST = 0, QT_SEG = 1 };
 #ifndef RR_SEEN
-#define RR_SEEN 16  // ghost-crossing distances remembered per (query, state) for the shared-edge dedup
+#define RR_SEEN 8  // ghost-crossing distances remembered per (query, state) for the shared-edge dedup
 #endif
 
 
@@ -37,8 +37,10 @@ struct __align__(16) Query {
   uint8_t type, want;    // want: bit F set -> evaluate state F
   uint8_t dyn_only, pad;
   // the ghost point x_G a T4 / T5 / T6 sample sent this ray / segment through (reading 12): a crossing
-  // at distance seed_t (> 0) with 1/|cos| = seed_ic that counts whether or not the (non-watertight) triangle test
-  // finds it; found hits within dedup_tol of it are the same crossing.  seed_t = 0: none.
+  // at distance seed_t (> 0) with 1/|cos| = seed_ic on ghost triangle eb that counts whether or not the
+  // (non-watertight) triangle test finds it; a found hit of triangle eb, or within dedup_tol of seed_t, is the
+  // same crossing.  seed_t = 0: none.  (eb is otherwise the excluded end triangle of a QT_SEG query; seeded
+  // segments only serve crossings.)
   float seed_t, seed_ic;
 };
 
@@ -200,7 +202,6 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
         if (seen_state != F) {
           ns = 0;
           seen_state = F;
-          if (q.seed_t > 0.0f) seen[ns++] = q.seed_t;
         }
       }
     }
@@ -208,6 +209,7 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
     WRay wr = make_wray(o, d);
     traverse<COUNT>(S, root, wr, tmin, tmax, [&](int li, float t, float tm, int id) -> float {
       if (kind == 2) {  // ghost crossing (all hits, dedup within dedup_tol)
+        if (q.seed_t > 0.0f && (id == q.eb || fabsf(t - q.seed_t) < S.dedup_tol)) return tm;  // the seeded one
         for (int a = 0; a < min(ns, RR_SEEN); ++a)
           if (fabsf(seen[a] - t) < S.dedup_tol) return tm;
         if (ns < RR_SEEN) seen[ns] = t;

@@ -84,9 +84,10 @@ struct SState {
 
 __device__ __forceinline__ bool nee_ok(int tech, int m) { return tech == 2 ? m >= 2 : true; }
 // the sample's own ghost crossing on the queried edge (Query::seed_t; reading 12)
-__device__ __forceinline__ Query seeded(Query q, float t, float3 nG) {
+__device__ __forceinline__ Query seeded(Query q, float t, const PV& xg) {
   q.seed_t = t;
-  q.seed_ic = 1.0f / fabsf(dot3(nG, q.d));
+  q.seed_ic = 1.0f / fabsf(dot3(xg.n, q.d));
+  q.eb = xg.tri;
   return q;
 }
 
@@ -120,7 +121,7 @@ __device__ void start_issue(const DevScene& S, int tech, int F, const float d0[8
       if (!(s.dl > S.eps)) return;
       s.dir = dv * (1.0f / s.dl);
       if (!(dot3(s.a.n, s.dir) > 0.0f)) return;
-      s.qi = B.push(seeded(mk_ray(s.a.p, s.dir, s.a.tri, bit(F)), s.dl, xg.n));
+      s.qi = B.push(seeded(mk_ray(s.a.p, s.dir, s.a.tri, bit(F)), s.dl, xg));
       return;
     }
     case 5: {  // ghost from sensor
@@ -131,7 +132,7 @@ __device__ void start_issue(const DevScene& S, int tech, int F, const float d0[8
       float3 dv = sub3(xg.p, E.p);
       s.dl = sqrtf(dot3(dv, dv));
       s.dir = dv * (1.0f / s.dl);
-      s.qi = B.push(seeded(mk_ray(E.p, s.dir, -1, bit(F)), s.dl, xg.n));
+      s.qi = B.push(seeded(mk_ray(E.p, s.dir, -1, bit(F)), s.dl, xg));
       return;
     }
   }
@@ -448,10 +449,11 @@ __device__ __forceinline__ bool single_step(const DevScene& S, const KArgs& A, S
         int pix = (int)(st.i % (uint64_t)npix);
         st.sp.dir = camera_dir(S, (float)(pix % S.W) + d0[0], (float)(pix / S.W) + d0[1]);
         st.sp.pix = st.sq.pix = pix;
-        st.sp.qi = st.sq.qi = B.push(mk_ray(p3(S.cam_pos), st.sp.dir, -1, 3));
+        st.sp.qi = st.sq.qi = B.push(mk_ray(p3(S.cam_pos), st.sp.dir, -1, A.nopm ? bit(F) : 3));
       } else {
         start_issue(S, A.tech, F, d0, st.sp, B);
-        start_issue(S, A.tech_q, Fb, d0, st.sq, B);
+        st.sq.qi = -1;
+        if (!A.nopm) start_issue(S, A.tech_q, Fb, d0, st.sq, B);  // no mapped path without path mapping
       }
       st.pc = 1;
       if (B.n > 0) return true;
@@ -464,7 +466,7 @@ __device__ __forceinline__ bool single_step(const DevScene& S, const KArgs& A, S
         st.P.pixel = st.Q.pixel = st.sp.pix;
         const QRes& r = B.r[st.sp.qi];
         if (r.ok[F]) { st.P.v[0] = E; st.P.v[1] = hit_pv(S, r.h[F], E.p, st.sp.dir, F); st.P.ex[1] = r.c[F]; st.P.n = 1; }
-        if (r.ok[Fb]) { st.Q.v[0] = E; st.Q.v[1] = hit_pv(S, r.h[Fb], E.p, st.sp.dir, Fb); st.Q.ex[1] = r.c[Fb]; st.Q.n = 1; }
+        if (r.ok[Fb] && !A.nopm) { st.Q.v[0] = E; st.Q.v[1] = hit_pv(S, r.h[Fb], E.p, st.sp.dir, Fb); st.Q.ex[1] = r.c[Fb]; st.Q.n = 1; }
       } else {
         start_consume(S, A.tech, F, st.sp, B, st.P);
         start_consume(S, A.tech_q, Fb, st.sq, B, st.Q);
@@ -523,12 +525,14 @@ struct BState {
   BPath P, Q;
 };
 
-__device__ void bidir_start_issue(const DevScene& S, const KArgs& A, int tech, int F, const Rng& rng, BPath& G, Batch& B) {
+__device__ void bidir_start_issue(const DevScene& S, const KArgs& A, int tech, int F, const Rng& rng, BPath& G, Batch& B,
+                                  bool skip = false) {
   G.ok = false;
   G.q0 = G.q1 = G.qyz = -1;
   G.A.n = G.B.n = G.A.nconn = G.B.nconn = 0;
   G.A.ended = G.B.ended = false;
   G.A.qw = G.B.qw = G.A.qc = G.B.qc = -1;
+  if (skip) return;  // the mapped path of RR_NO_PATH_MAPPING: none
   const int D = A.max_depth;
   float d0[8];
   rng.dims(0, d0);
@@ -587,7 +591,7 @@ __device__ void bidir_issue(const DevScene& S, const KArgs& A, int tech, int F, 
     Query q = mk_seg(G.A.v[0].p, G.A.v[1].p, -2, -2, bit(F));
     const P3 a = G.A.v[0].p;
     const double gx = G.start.p.x - a.x, gy = G.start.p.y - a.y, gz = G.start.p.z - a.z;
-    G.qyz = B.push(seeded(q, (float)sqrt(gx * gx + gy * gy + gz * gz), G.start.n));
+    G.qyz = B.push(seeded(q, (float)sqrt(gx * gx + gy * gy + gz * gz), G.start));
   }
   PV E = cam_pv(S);
   for (int side = 0; side < 2; ++side) {
@@ -747,7 +751,7 @@ __device__ bool bidir_step(const DevScene& S, const KArgs& A, BState& st, Batch&
       B.n = 0;
       st.nmax = l == 3 ? A.max_depth - 3 : A.max_depth - 2;
       bidir_start_issue(S, A, l, F, st.rng, st.P, B);
-      bidir_start_issue(S, A, l, Fb, st.rng, st.Q, B);
+      bidir_start_issue(S, A, l, Fb, st.rng, st.Q, B, A.nopm != 0);
       st.pc = 1;
       if (B.n > 0) return true;
       continue;

@@ -116,7 +116,8 @@ __device__ __forceinline__ float area_pdf(const DevScene& S, int F, const PV& pr
 // ------------------------------------------------------------------------------------------------
 // value of a connection path v = f / Pi (Eq.2; balance heuristic P:L351-353), in state F.
 // x[0] = E, x[k-1] = L; e[i] = crossings of edge (x_i, x_{i+1}) with sa measured from x_i, sb from x_{i+1}.
-// Computed as (f / p_T7) / (1 + sum_c p_c / p_T7).
+// Computed as (f / p_T7) / (1 + sum_c p_c / p_T7).  mask bit 8 (RR_NO_PATH_MAPPING): a static path (no vertex
+// on an edited object, no ghost crossing on any edge) has value 0.
 // ------------------------------------------------------------------------------------------------
 __device__ inline float3 path_value(const DevScene& S, const PV* x, const Cross* e, int k, int F, uint32_t mask) {
   const float3 zero = f3(0.f, 0.f, 0.f);
@@ -129,7 +130,9 @@ __device__ inline float3 path_value(const DevScene& S, const PV* x, const Cross*
   float4 le4 = __ldg(&S.obj_emit[L.obj]);
   float3 Le = f3(le4.x, le4.y, le4.z);
   if (!(dot3(L.n, sub3(x[k - 2].p, L.p)) > 0.0f)) return zero;  // front face only
-  if (k == 2) return Le;                                     // direct view: W_e G / p_cam = 1, Pi = p_T7
+  const bool reject_static = (mask & 0x100u) != 0;
+  bool dyn_any = e[0].n > 0.0f;
+  if (k == 2) return (reject_static && !dyn_any) ? zero : Le;  // direct view: W_e G / p_cam = 1, Pi = p_T7
   float cos1 = fabsf(dot3(x[1].n, w01));
   float invpcam = S.Aplane * cth * cth * cth * dd01 / cos1;  // 1 / p_cam(x_1)
   float pL = __ldg(&S.emit_pL[__ldg(&S.obj_emitter[L.obj])]);
@@ -149,6 +152,7 @@ __device__ inline float3 path_value(const DevScene& S, const PV* x, const Cross*
     float cout = fabsf(dot3(x[i].n, wo));
     float cin_next = fabsf(dot3(x[i + 1].n, wo));
     bool dyn = edited(S, x[i].obj);
+    dyn_any = dyn_any || dyn || e[i].n > 0.0f;
     if (!(pf > 0.0f)) return zero;  // f = 0 (rho = 0 exactly where pf = 0 for these BSDFs)
     if (i < k - 2) {
       T = mul3(T, rho * (cout / pf));
@@ -171,6 +175,7 @@ __device__ inline float3 path_value(const DevScene& S, const PV* x, const Cross*
       Q *= pr * cout / (pf * cin_next);
     }
   }
+  if (reject_static && !dyn_any) return zero;
   return T * (1.0f / sum);
 }
 

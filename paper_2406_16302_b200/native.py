@@ -15,6 +15,8 @@ RR_OK, RR_E_INVALID, RR_E_STATE, RR_E_CUDA, RR_E_OOM = 0, -1, -2, -3, -4
 RR_TWO_WAY, RR_RECONNECT, RR_REJECT_MULTI, RR_ACCUMULATE, RR_COUNT_TRAVERSAL = 1, 2, 4, 8, 16
 RR_VNDF = 32
 RR_DIAG_ONE_WAY_ABLATION = 64  # diagnostic, deliberately biased (include/rr.h)
+RR_PRIMAL_SHARED_STREAMS = 128  # rr_render_primal: one stream for both states
+RR_NO_PATH_MAPPING = 256  # "incremental w/o PM" ablation (include/rr.h)
 
 
 class rr_material(C.Structure):

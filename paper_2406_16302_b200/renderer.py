@@ -137,8 +137,9 @@ class Renderer:
         return image
 
     def render_primal(self, state: int, spp: int, seed: int, max_depth: int, image=None, stream: Optional[int] = None,
-                      count_traversal: bool = False):
-        """Primal image I^D(state) (state 0 = new, 1 = old) into a torch float32 (H, W, 4) CUDA tensor."""
+                      count_traversal: bool = False, shared_streams: bool = False):
+        """Primal image I^D(state) (state 0 = new, 1 = old) into a torch float32 (H, W, 4) CUDA tensor.
+        shared_streams: the same random numbers in both states (correlated primal difference)."""
         import torch
         if image is None:
             image = torch.empty((self.height, self.width, 4), dtype=torch.float32, device=f"cuda:{self.device}")
@@ -146,7 +147,7 @@ class Renderer:
         assert tuple(image.shape) == (self.height, self.width, 4)
         if stream is None:
             stream = torch.cuda.current_stream(self.device).cuda_stream
-        flags = N.RR_COUNT_TRAVERSAL if count_traversal else 0
+        flags = (N.RR_COUNT_TRAVERSAL if count_traversal else 0) | (N.RR_PRIMAL_SHARED_STREAMS if shared_streams else 0)
         self._check(self._L.rr_render_primal(self.h, int(state), int(spp), int(seed), int(max_depth), flags,
                                              image.data_ptr(), int(stream)), "rr_render_primal")
         return image

@@ -38,6 +38,7 @@ ACCUMULATE = 8
 PAPER_FLAGS = TWO_WAY | RECONNECT | REJECT_MULTI
 VNDF = 32  # GGX directions from the visible normals (Heitz 2018), both implementations
 DIAG_ONE_WAY = 64  # RR_DIAG_ONE_WAY_ABLATION: one-way with the two-way pairing rules (biased test mode)
+NO_PATH_MAPPING = 256  # RR_NO_PATH_MAPPING: "incremental w/o PM", with TWO_WAY
 
 
 @dataclasses.dataclass
@@ -588,6 +589,77 @@ def occluder_reveal(width: int = 32, height: int = 32, spp: int = 4, max_depth: 
     c0 = np.array([0.25, 0.1, 0.5])
     ed = Edit(cube, translate_xform(c0), translate_xform(c0 + np.array([0.45, 0.0, 0.0])))
     return Workload(scene, [ed], RenderArgs(spp=spp, seed=7, max_depth=max_depth), name="occluder-reveal")
+
+
+# ----------------------------------------------------------------------------------------
+# Sweeps of the paper's Table num_of_dynamics and Table material_editing, on the
+# Cornell stand-ins (the paper's own scenes are not available).  Displacements scale the paper's 40/100/160/220
+# units on its ~550-unit Cornell box to the unit box: 0.073 / 0.18 / 0.29 / 0.40.
+# ----------------------------------------------------------------------------------------
+DISPLACEMENT_LADDER = (0.073, 0.18, 0.29, 0.40)
+
+
+def cornell_dynamics(n_dyn: int, displacement: float = 0.1, width: int = 64, height: int = 64, spp: int = 4,
+                     max_depth: int = 4, seed: int = 0) -> Workload:
+    """n_dyn small cubes (side 0.12) scattered uniformly over the Cornell box (seeded, non-overlapping, clear of
+    the static block and the light), each moved by `displacement` in a random horizontal direction ("we
+    uniformly scatter eight moving objects across the scene")."""
+    rng = np.random.Generator(np.random.Philox(key=0x5EED0100 + n_dyn))
+    b = _Builder()
+    gray = _cornell_room(b)
+    h = 0.06
+    placed, edits = [], []
+    while len(placed) < n_dyn:
+        c = rng.uniform([0.08, 0.07, 0.08], [0.92, 0.85, 0.92])
+        c[1] = max(c[1], h + 0.001)
+        d = rng.normal(size=2)
+        d = d / np.linalg.norm(d) * displacement
+        c2 = c + np.array([d[0], 0.0, d[1]])
+        sep = 2 * h + 0.01  # boxes (old and new placements) never overlap another cube's
+        ok = all(np.max(np.abs(a - q)) > sep for p, p2 in placed for a in (c, c2) for q in (p, p2))
+        inside = np.all(c2 > h + 0.01) and np.all(c2 < 1 - h - 0.01) and c2[1] == c[1]
+        block = lambda x: (0.55 - h < x[0] < 0.85 + h) and (x[1] < 0.6 + h) and (x[2] > 0.7 - h)  # noqa: E731
+        if ok and inside and not block(c) and not block(c2):
+            placed.append((c, c2))
+            obj = b.add(*box((-h, -h, -h), (h, h, h)), gray, flags=OBJ_DYNAMIC)
+            edits.append(Edit(obj, translate_xform(c), translate_xform(c2)))
+    scene = b.build(Camera(width=width, height=height, **CORNELL_CAMERA), 1e-4, f"cornell-{n_dyn}dyn")
+    return Workload(scene, edits, RenderArgs(spp=spp, seed=seed, max_depth=max_depth), name=f"dynamics{n_dyn}")
+
+
+def cornell_displacement(d: float, width: int = 64, height: int = 64, spp: int = 4, max_depth: int = 4,
+                         seed: int = 0) -> Workload:
+    """config 1's cube moved by d along +x (Table num_of_dynamics (b), the displacement ladder)"""
+    w = config1(width, height, spp, max_depth, seed)
+    w.edits = [Edit(w.edits[0].object, translate_xform(CUBE_CENTER), translate_xform(CUBE_CENTER + np.array([d, 0, 0])))]
+    w.name = f"displacement{d:g}"
+    return w
+
+
+MATERIAL_EDITS = ("white_to_blue", "ggx_0.1_to_0.5", "lambert_to_metallic")
+
+
+def cornell_material_edit(kind: str, width: int = 64, height: int = 64, spp: int = 4, max_depth: int = 6,
+                          seed: int = 2) -> Workload:
+    """Table material_editing's three edits on config 2's scene (sphere + cube), one at a time:
+    the sphere's Lambert white -> blue; the cube's GGX roughness 0.1 -> 0.5; the sphere Lambert -> metallic
+    (GGX, F0 0.9, alpha 0.2)."""
+    w = config2(width, height, spp, max_depth, seed)
+    cube_e, sph_e = w.edits
+    if kind == "white_to_blue":
+        e = dataclasses.replace(sph_e, old_material=Material(LAMBERT, (0.8, 0.8, 0.8)),
+                                new_material=Material(LAMBERT, (0.1, 0.1, 0.8)))
+    elif kind == "ggx_0.1_to_0.5":
+        e = dataclasses.replace(cube_e, old_material=Material(GGX, (0.8, 0.8, 0.8), 0.1),
+                                new_material=Material(GGX, (0.8, 0.8, 0.8), 0.5))
+    elif kind == "lambert_to_metallic":
+        e = dataclasses.replace(sph_e, old_material=Material(LAMBERT, (0.8, 0.8, 0.8)),
+                                new_material=Material(GGX, (0.9, 0.9, 0.9), 0.2))
+    else:
+        raise ValueError(kind)
+    w.edits = [e]
+    w.name = f"material-{kind}"
+    return w
 
 
 def subsample(w: Workload, width: int, height: int) -> Workload:

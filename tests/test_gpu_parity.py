@@ -303,6 +303,17 @@ def test_records_diag_one_way_config1(torch_cuda):
     record_parity(w, args)
 
 
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_records_no_path_mapping(torch_cuda, cfg):
+    """RR_NO_PATH_MAPPING ("incremental w/o PM"): every connection unpaired, static paths rejected."""
+    w = S.config1() if cfg == 1 else S.load_config(cfg)
+    args = dataclasses.replace(w.args, flags=S.TWO_WAY | S.NO_PATH_MAPPING)
+    if cfg == 1:
+        record_parity(w, args)
+    else:
+        record_parity(w, args, n_per=1024, strided=True)
+
+
 def test_records_config5_late_frame(torch_cuda):
     """Config 5, frame 11 (edits S_11 -> S_12, seed 5000 + 11): every object has moved by 11 steps."""
     w = S.config5()
@@ -451,8 +462,9 @@ def test_invalid_arguments_are_refused(torch_cuda):
     w = S.config1(16, 16)
     r = _renderer(w)
     for bad in (dict(technique_mask=0x3F), dict(spp=3), dict(max_depth=0), dict(max_depth=11),
-                dict(flags=S.RECONNECT), dict(layer_mask=0x80), dict(flags=S.PAPER_FLAGS | 128),
-                dict(flags=S.PAPER_FLAGS | S.DIAG_ONE_WAY)):
+                dict(flags=S.RECONNECT), dict(layer_mask=0x80), dict(flags=S.PAPER_FLAGS | 512),
+                dict(flags=S.PAPER_FLAGS | S.DIAG_ONE_WAY), dict(flags=S.PAPER_FLAGS | S.NO_PATH_MAPPING),
+                dict(flags=S.NO_PATH_MAPPING)):
         with pytest.raises(RRError):
             r.render_residual(dataclasses.replace(w.args, **bad))
     for bad in (dict(state=2), dict(spp=0), dict(max_depth=0), dict(max_depth=11)):
@@ -481,6 +493,25 @@ def test_primal_image_matches_oracle(torch_cuda, cfg, W, spp, D):
         assert scale > 0
         rmse = math.sqrt(((g - ref) ** 2).mean())
         assert rmse <= 1e-3 * scale, (F, rmse, scale)
+
+
+def test_correlated_primal_difference_matches_oracle(torch_cuda):
+    """RR_PRIMAL_SHARED_STREAMS: primal(new) - primal(old) with one random stream for both states, against the
+    oracle's correlated primal difference on the same streams (the quality harness's reference)."""
+    torch = torch_cuda
+    from paper_2406_16302_b200 import RRError
+    w = S.config1(32, 32, spp=4, max_depth=4)
+    r = _renderer(w)
+    o = _oracle(w)
+    g = (r.render_primal(0, 64, 9, 4, shared_streams=True).clone() - r.render_primal(1, 64, 9, 4, shared_streams=True))
+    g = g[..., :3].double().cpu().numpy()
+    ref = o.primal_difference(9, 64, 4)
+    scale = np.abs(ref).max()
+    assert scale > 0
+    assert math.sqrt(((g - ref) ** 2).mean()) <= 1e-3 * scale
+    img = torch.empty((32, 32, 4), dtype=torch.float32, device="cuda")
+    with pytest.raises(RRError):  # unknown primal flag bits
+        r._check(r._L.rr_render_primal(r.h, 0, 4, 1, 4, 1 << 12, img.data_ptr(), 0), "rr_render_primal")
 
 
 def test_technique_layers_sum_to_full_render(torch_cuda):
