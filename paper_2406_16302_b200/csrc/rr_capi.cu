@@ -166,6 +166,16 @@ rr_status rr_scene_upload(rr_ctx* c, const rr_scene_desc* d) {
     if (ob.flags & RR_OBJ_DYNAMIC) n_dyn++;
   }
   if (n_emit_obj == 0) return fail(c, RR_E_INVALID, "scene has no emitter");
+  {  // an emitter or dynamic object without triangles would give p_L = 1/0 or an empty BLAS: refuse it
+    std::vector<uint32_t> cnt(O, 0);
+    for (uint32_t k = 0; k < T; ++k) cnt[d->tri_object[k]]++;
+    for (uint32_t o = 0; o < O; ++o) {
+      const rr_object& ob = d->objects[o];
+      bool emits = ob.emission[0] > 0 || ob.emission[1] > 0 || ob.emission[2] > 0;
+      if (cnt[o] == 0 && (emits || (ob.flags & RR_OBJ_DYNAMIC)))
+        return fail(c, RR_E_INVALID, "emitting or dynamic object " + std::to_string(o) + " has no triangles");
+    }
+  }
   if (n_dyn > RR_MAX_INST) return fail(c, RR_E_INVALID, "too many dynamic objects (max 8)");
   for (uint32_t m = 0; m < M; ++m) {
     const rr_material& mt = d->materials[m];
@@ -566,6 +576,8 @@ rr_status rr_set_edit(rr_ctx* c, uint32_t n, const rr_edit* edits) {
     if (moved && (ob.emission[0] > 0 || ob.emission[1] > 0 || ob.emission[2] > 0))
       return fail(c, RR_E_INVALID, "moved objects must not emit");
   }
+  // the previous render may still read the per-state tables on its stream: wait for its last event only
+  if (c->ev_init && c->n_ev > 0) cudaEventSynchronize(c->ev[c->n_ev - 1]);
   try {
     DevScene& S = c->S;
     std::vector<rr_material> mats = c->materials;
@@ -642,13 +654,13 @@ rr_status rr_set_edit(rr_ctx* c, uint32_t n, const rr_edit* edits) {
       m4[k] = make_float4(mats[k].albedo[0], mats[k].albedo[1], mats[k].albedo[2], mats[k].roughness);
       mt[k] = mats[k].type;
     }
-    c->mat.upload(m4.data(), m4.size());
-    c->mat_type.upload(mt.data(), mt.size());
+    c->mat.upload_reuse(m4.data(), m4.size());
+    c->mat_type.upload_reuse(mt.data(), mt.size());
     for (auto& t : mt) t = t == RR_GGX ? 2u : t;  // RR_VNDF renders: GGX sampled from the visible normals
-    c->mat_type_vndf.upload(mt.data(), mt.size());
-    c->obj_mat0.upload(om0.data(), O);
-    c->obj_mat1.upload(om1.data(), O);
-    c->obj_flags.upload(flags.data(), O);
+    c->mat_type_vndf.upload_reuse(mt.data(), mt.size());
+    c->obj_mat0.upload_reuse(om0.data(), O);
+    c->obj_mat1.upload_reuse(om1.data(), O);
+    c->obj_flags.upload_reuse(flags.data(), O);
     S.mat = c->mat.p;
     S.mat_type = c->mat_type.p;
     S.obj_mat[0] = c->obj_mat0.p;
@@ -659,8 +671,8 @@ rr_status rr_set_edit(rr_ctx* c, uint32_t n, const rr_edit* edits) {
     if (!moved_tris.empty()) {
       std::vector<float> cd;
       double area = build_cdf(c, moved_tris, cd);
-      c->moved_tris.upload(moved_tris.data(), moved_tris.size());
-      c->moved_cdf.upload(cd.data(), cd.size());
+      c->moved_tris.upload_reuse(moved_tris.data(), moved_tris.size());
+      c->moved_cdf.upload_reuse(cd.data(), cd.size());
       S.n_moved = (int)moved_tris.size();
       S.moved_tris = c->moved_tris.p;
       S.moved_cdf = c->moved_cdf.p;

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "rr_device.cuh"
 #include "rr_kernels.h"
@@ -117,13 +118,19 @@ __global__ void __launch_bounds__(RR_PRIMAL_BLOCK, 8) k_primal(const __grid_cons
 
 void launch_primal(const DevScene& S, int F, uint64_t seed, int D, uint32_t spp, float* image,
                    unsigned long long* stats, bool count, bool shared_streams, cudaStream_t st) {
-  static int grid = 0;
-  if (!grid) {
-    int dev = 0, sms = 148, occ = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_primal<false>, RR_PRIMAL_BLOCK, 0);
-    grid = sms * std::max(1, occ);
+  static int grids[64] = {0};  // per device
+  static std::mutex mu;
+  int dev = 0, grid = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!grids[dev & 63]) {
+      int sms = 148, occ = 1;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_primal<false>, RR_PRIMAL_BLOCK, 0);
+      grids[dev & 63] = sms * std::max(1, occ);
+    }
+    grid = grids[dev & 63];
   }
   uint64_t n = (uint64_t)S.W * S.H * spp;
   int g = (int)std::min<uint64_t>((uint64_t)grid, (n + RR_PRIMAL_BLOCK - 1) / RR_PRIMAL_BLOCK);

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "rr_device.cuh"
 #include "rr_kernels.h"
@@ -994,16 +995,25 @@ __global__ void k_segment(const __grid_constant__ DevScene S, uint32_t n, const 
 // ---- host launchers
 // persistent lanes: one wave of resident blocks on every SM (fewer for tiny launches)
 int residual_grid(bool bidir, uint64_t n) {
-  static int occ[2] = {0, 0}, sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], kplain::k_residual_single<false>, RR_BLOCK, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], kplain::k_residual_bidir<false>, RR_BLOCK, 0);
+  // SM count and occupancy per device (a process may drive several GPUs, one context each)
+  struct Dev { int sms = 0, occ[2] = {0, 0}; };
+  static Dev cache[64];
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Dev d;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    Dev& c = cache[dev & 63];
+    if (!c.sms) {
+      cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ[0], kplain::k_residual_single<false>, RR_BLOCK, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ[1], kplain::k_residual_bidir<false>, RR_BLOCK, 0);
+    }
+    d = c;
   }
   uint64_t g = (n + RR_BLOCK - 1) / RR_BLOCK;
-  uint64_t cap = (uint64_t)sms * (uint64_t)std::max(1, occ[bidir ? 1 : 0]);
+  uint64_t cap = (uint64_t)d.sms * (uint64_t)std::max(1, d.occ[bidir ? 1 : 0]);
   return (int)std::max<uint64_t>(1, std::min(g, cap));
 }
 int residual_block() { return RR_BLOCK; }

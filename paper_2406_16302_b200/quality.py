@@ -1,17 +1,25 @@
-"""Equal-budget quality harness (SURVEY 8(f) row 1; the paper's comparison protocol, P:L504-519).
+"""Equal-budget quality harness (SURVEY 8(f) row 1; the paper's comparison protocol, P:L504-519, P:L559-639).
 
-Estimators of the residual Delta = I(new) - I(old) compared against a high-sample reference:
-  * "pt_difference"   -- path tracing from scratch in each state with independent seeds;
-  * "correlated_pt"   -- camera paths only (T7), random-number replay in both states (mask {7}, one-way;
-                         P:L510-511);
-  * "residual"        -- the paper's method: all seven techniques, path mapping, two-way;
-ablations of the method (the mapping components of P:L387-436, one at a time):
-  * "residual_replay" -- two-way, no reconnection: diverged paths are replayed only (RR_RECONNECT off);
-  * "residual_one_way"-- one side per technique, replay only (flags 0; SPEC's "mapping off" run knob);
-and the paper's mode with GGX visible-normal sampling ("residual_vndf", RR_VNDF).
-Each is timed with CUDA events on the device; mse() and ssim() are taken against the reference and
-efficiency = 1 / (mse * seconds).  Scenes are the synthetic stand-ins of rr_inputs (no
-measured data).
+Estimators of the residual Delta = I(new) - I(old):
+  * "pt_difference"    -- path tracing from scratch in each state with independent seeds;
+  * "correlated_pt"    -- camera paths only (T7), random-number replay in both states (mask {7}, one-way;
+                          P:L510-511);
+  * "residual"         -- the paper's method: all seven techniques, path mapping, two-way;
+ablations of the method:
+  * "residual_no_pm"   -- "incremental w/o PM" (Table num_of_dynamics): both states sampled by the
+                          dynamic techniques separately, no path mapping (RR_NO_PATH_MAPPING);
+  * "residual_replay"  -- two-way, no reconnection: diverged paths are replayed only (RR_RECONNECT off);
+  * "residual_one_way" -- one side per technique, replay only (flags 0; SPEC's "mapping off" run knob);
+  * "residual_vndf"    -- the paper's mode with GGX visible-normal sampling (RR_VNDF).
+
+The reference is NOT any of these estimators: it is the GPU primal renderer (unidirectional NEE/BSDF-MIS path
+tracing, rr_primal.cu, pinned to the oracle's primal renderer) run in both states with the SAME random numbers
+(RR_PRIMAL_SHARED_STREAMS) at high spp -- a correlated, unbiased estimate of I(new) - I(old) that shares no code
+with the residual estimator.  Its own variance is estimated from its chunks and subtracted from every MSE
+(mse = mean |x - ref|^2 - var(ref)), so a reference noisier than intended cannot flatter or hurt an estimator.
+Every estimator is timed with CUDA events on the device; efficiency = 1 / (mse * seconds), and the
+MSE "at equal time" of estimator e against the paper's residual = mse_e * t_e / t_residual (the paper's tables).
+Scenes are the synthetic stand-ins of rr_inputs (no measured data).
 """
 from __future__ import annotations
 
@@ -21,6 +29,7 @@ from typing import Dict
 import numpy as np
 
 PAPER_FLAGS = 7
+NO_PATH_MAPPING = 256
 
 
 def _timed(fn):
@@ -34,14 +43,24 @@ def _timed(fn):
     return img[..., :3].double().cpu().numpy(), e0.elapsed_time(e1) / 1e3
 
 
-def reference(r, args, spp: int = 1024, seed: int = 1 << 20) -> np.ndarray:
-    """High-sample residual (all techniques, two-way) on seeds disjoint from every estimator below.  Unbiased
-    (record-level parity with the CPU reference implementation, whose residual converges to I(new) - I(old) in
-    its tests), and its variance is far below a path-traced difference of the same spp, which would dominate
-    every MSE."""
-    a = dataclasses.replace(args, spp=spp + (spp & 1), seed=seed, flags=PAPER_FLAGS)
-    img, _ = _timed(lambda: r.render_residual(a).clone())
-    return img
+def reference(r, args, spp: int = 65536, chunk: int = 4096, seed: int = 1 << 20):
+    """(mean, variance of the mean per pixel) of the correlated primal difference primal(N) - primal(O) at `spp`
+    samples per pixel, in chunks of `chunk` spp with distinct seeds."""
+    imgs = []
+    for k in range(max(1, spp // chunk)):
+        img, _ = _timed(lambda: r.render_primal(0, chunk, seed + k, args.max_depth, shared_streams=True).clone()
+                        - r.render_primal(1, chunk, seed + k, args.max_depth, shared_streams=True))
+        imgs.append(img)
+    a = np.stack(imgs)
+    return a.mean(0), (a.var(0) / len(a) if len(a) > 1 else np.zeros_like(a[0]))
+
+
+def reference_primal(r, state: int, max_depth: int, spp: int = 16384, chunk: int = 4096, seed: int = 3 << 20):
+    """(mean, variance of the mean) of primal(state) at `spp` spp: the reference of PT from scratch"""
+    imgs = [_timed(lambda: r.render_primal(state, chunk, seed + k, max_depth).clone())[0]
+            for k in range(max(1, spp // chunk))]
+    a = np.stack(imgs)
+    return a.mean(0), (a.var(0) / len(a) if len(a) > 1 else np.zeros_like(a[0]))
 
 
 def estimators(r, args, spp: int, seed: int = 0, ablations: bool = False) -> Dict[str, tuple]:
@@ -53,6 +72,8 @@ def estimators(r, args, spp: int, seed: int = 0, ablations: bool = False) -> Dic
     out["correlated_pt"] = _timed(lambda: r.render_residual(corr).clone())
     full = dataclasses.replace(args, spp=spp + (spp & 1), seed=seed + 14, flags=PAPER_FLAGS)
     out["residual"] = _timed(lambda: r.render_residual(full).clone())
+    nopm = dataclasses.replace(full, seed=seed + 18, flags=1 | NO_PATH_MAPPING)
+    out["residual_no_pm"] = _timed(lambda: r.render_residual(nopm).clone())
     if ablations:
         rep = dataclasses.replace(full, seed=seed + 15, flags=PAPER_FLAGS & ~2)
         out["residual_replay"] = _timed(lambda: r.render_residual(rep).clone())
@@ -63,8 +84,11 @@ def estimators(r, args, spp: int, seed: int = 0, ablations: bool = False) -> Dic
     return out
 
 
-def mse(img: np.ndarray, ref: np.ndarray) -> float:
-    return float(((img - ref) ** 2).mean())
+def mse(img: np.ndarray, ref, ref_var=None) -> float:
+    """mean squared error against the reference, minus the reference's own variance (unbiased for the error
+    of `img` when the reference's noise is independent of it)"""
+    m = float(((img - ref) ** 2).mean())
+    return m - float(ref_var.mean()) if ref_var is not None else m
 
 
 def _box(a: np.ndarray, k: int) -> np.ndarray:
@@ -85,11 +109,64 @@ def ssim(img: np.ndarray, ref: np.ndarray, k: int = 7) -> float:
     return float(s.mean())
 
 
-def compare(r, args, spp: int, ref: np.ndarray, seed: int = 0, ablations: bool = False) -> Dict[str, dict]:
+def compare(r, args, spp: int, ref, seed: int = 0, ablations: bool = False) -> Dict[str, dict]:
+    """ref = (mean, variance of the mean) from reference()"""
+    ref_mean, ref_var = ref
     res = {}
     estimators(r, args, spp, seed + 1000, ablations)  # warm-up: first launches of each kernel are not timed
     for name, (img, sec) in estimators(r, args, spp, seed, ablations).items():
-        m = mse(img, ref)
-        res[name] = {"mse": m, "ssim": ssim(img, ref), "seconds": sec,
+        m = mse(img, ref_mean, ref_var)
+        res[name] = {"mse": m, "ssim": ssim(img, ref_mean), "seconds": sec,
                      "efficiency": 1.0 / (m * sec) if m > 0 and sec > 0 else float("inf")}
+    t0 = res["residual"]["seconds"]
+    for v in res.values():
+        v["mse_at_residual_time"] = v["mse"] * v["seconds"] / t0
+    res["_reference"] = {"variance_of_mean": float(ref_var.mean()), "max_abs": float(np.abs(ref_mean).max())}
+    return res
+
+
+def technique_variance(r, args, spp: int, n_seeds: int = 16, seed: int = 500) -> Dict[int, dict]:
+    """Per technique l: the variance its MIS-weighted layer adds to the residual (mean over pixels of the
+    per-pixel variance over n_seeds renders; the layers of different techniques are independent), and its
+    device time per render.  Shows which technique's samples the estimator's noise and cost come from."""
+    import torch
+    layers = {}
+    times = {}
+    a0 = dataclasses.replace(args, spp=spp + (spp & 1), flags=PAPER_FLAGS)
+    for k in range(n_seeds):
+        a = dataclasses.replace(a0, seed=seed + k)
+        for l in range(1, 8):
+            if not (int(a.technique_mask) >> (l - 1)) & 1:
+                continue
+            img, sec = _timed(lambda: r.render_residual(dataclasses.replace(a, layer_mask=1 << (l - 1))).clone())
+            layers.setdefault(l, []).append(img)
+            times.setdefault(l, []).append(sec)
+    torch.cuda.synchronize()
+    out = {}
+    tot_var = sum(float(np.stack(v).var(0).mean()) for v in layers.values())
+    tot_t = sum(float(np.median(t)) for t in times.values())
+    for l, v in layers.items():
+        var = float(np.stack(v).var(0).mean())
+        t = float(np.median(times[l]))
+        out[l] = {"variance": var, "variance_share": var / tot_var if tot_var > 0 else 0.0, "seconds": t,
+                  "time_share": t / tot_t if tot_t > 0 else 0.0,
+                  "mean_abs": float(np.abs(np.stack(v).mean(0)).mean())}
+    return out
+
+
+def sweep_row(r, w, spp: int, ref_spp: int = 65536, pt_ref_spp: int = 16384) -> dict:
+    """One row of the paper's Table num_of_dynamics / Table material_editing: MSE at equal time (the paper's
+    residual's time) and SSIM of PT from scratch (of the NEW image against its own high-spp reference),
+    correlated PT, incremental w/o PM and incremental w/ PM (residuals: I_new = I_old + Delta with a converged
+    I_old, so the error of I_new is the error of Delta)."""
+    args = w.args
+    ref = reference(r, args, ref_spp)
+    res = compare(r, args, spp, ref)
+    new_mean, new_var = reference_primal(r, 0, args.max_depth, pt_ref_spp)
+    _timed(lambda: r.render_primal(0, spp, 77, args.max_depth))  # warm-up
+    img, sec = _timed(lambda: r.render_primal(0, spp, 78, args.max_depth).clone())
+    m = mse(img, new_mean, new_var)
+    res["pt_from_scratch"] = {"mse": m, "ssim": ssim(img, new_mean), "seconds": sec,
+                              "efficiency": 1.0 / (m * sec) if m > 0 else float("inf"),
+                              "mse_at_residual_time": m * sec / res["residual"]["seconds"]}
     return res
