@@ -153,9 +153,7 @@ typedef struct {
   uint64_t sched[8];       /* warp-scheduler occupancy of the residual kernels (diagnostics): [0] warp
                               rounds, [2] sample steps, [3] queries per round summed, [4] lanes holding
                               a sample summed over rounds, [5] deepest BVH root-to-leaf path in inner
-                              nodes (scene property; upload fails above RR_STACK = 64), [6] ghost
-                              crossings beyond the 8 remembered per (query, state) for the shared-edge dedup
-                              (counted, not deduplicated; 0 on the BASELINE scenes), ([1], [7] reserved, 0) */
+                              nodes (scene property; upload fails above RR_STACK = 64), ([1], [6..7] reserved, 0) */
 } rr_stats;
 
 /* one record per emitted base connection (C10), for parity tests */

@@ -34,6 +34,7 @@ __host__ __device__ __forceinline__ float3 cross3(float3 a, float3 b) {
   return f3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
 }
 __device__ __forceinline__ float3 norm3_exact(float3 a) { return a * (1.0f / sqrtf(dot3(a, a))); }
+__device__ __forceinline__ float norm3f(float3 a) { return sqrtf(dot3(a, a)); }
 __device__ __forceinline__ bool eq3(float3 a, float3 b) {
   return __float_as_uint(a.x) == __float_as_uint(b.x) && __float_as_uint(a.y) == __float_as_uint(b.y) &&
          __float_as_uint(a.z) == __float_as_uint(b.z);
@@ -368,7 +369,6 @@ __device__ __forceinline__ Cross cross_zero() { Cross c; c.n = c.s0 = c.sa = c.s
 
 struct QCount {  // per-thread query counters
   uint32_t closest, shadow, inst;
-  uint32_t seen_overflow;  // ghost crossings beyond RR_SEEN per (query, state): not deduplicated (rr_stats.sched[6])
   TCount tc;
 };
 

@@ -20,9 +20,6 @@
 namespace rr {
 
 enum { QT_CLOSEST = 0, QT_SEG = 1 };
-#ifndef RR_SEEN
-#define RR_SEEN 8  // ghost-crossing distances remembered per (query, state) for the shared-edge dedup
-#endif
 
 
 
@@ -36,12 +33,11 @@ struct __align__(16) Query {
   int ea, eb;            // excluded triangles (origin, end)
   uint8_t type, want;    // want: bit F set -> evaluate state F
   uint8_t dyn_only, pad;
-  // the ghost point x_G a T4 / T5 / T6 sample sent this ray / segment through (reading 12): a crossing
-  // at distance seed_t (> 0) with 1/|cos| = seed_ic on ghost triangle eb that counts whether or not the
-  // (non-watertight) triangle test finds it; a found hit of triangle eb, or within dedup_tol of seed_t, is the
-  // same crossing.  seed_t = 0: none.  (eb is otherwise the excluded end triangle of a QT_SEG query; seeded
-  // segments only serve crossings.)
-  float seed_t, seed_ic;
+  // x_G of a T4 / T5 / T6 sample on this ray / segment (reading 12): seed_t > 0 its distance, eb its
+  // ghost triangle.  The ghost-crossing jobs skip that crossing (a hit of triangle eb, or within dedup_tol of
+  // seed_t); the consumer adds it exactly (add_seed), so it counts once whether or not the non-watertight
+  // triangle test finds it.  seed_t = 0: none.  (For QT_SEG eb is otherwise the excluded end triangle.)
+  float seed_t;
 };
 
 struct __align__(16) QRes {
@@ -156,14 +152,8 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
   best_t[0] = best_t[1] = thi;
   bool blocked[2] = {false, false};
   bool sblock = false;
-  float seen[RR_SEEN];
+  float seen[8];
   int ns = 0, seen_state = -1;
-  if (q.seed_t > 0.0f) {  // the sample's own crossing (single-state query); its (L - t) term is added at the end
-    const int G = (q.want & 1) ? 0 : 1;
-    r.c[G].n = 1.0f;
-    r.c[G].s0 = q.seed_ic;
-    r.c[G].sa = q.seed_t * q.seed_t * q.seed_ic;
-  }
   const int NI = S.n_inst;
   const int njobs = 1 + 4 * NI;
   for (int j = 0; j < njobs; ++j) {
@@ -209,12 +199,10 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
     WRay wr = make_wray(o, d);
     traverse<COUNT>(S, root, wr, tmin, tmax, [&](int li, float t, float tm, int id) -> float {
       if (kind == 2) {  // ghost crossing (all hits, dedup within dedup_tol)
-        if (q.seed_t > 0.0f && (id == q.eb || fabsf(t - q.seed_t) < S.dedup_tol)) return tm;  // the seeded one
-        for (int a = 0; a < min(ns, RR_SEEN); ++a)
+        if (fabsf(t - q.seed_t) < S.dedup_tol || (id == q.eb && q.seed_t > 0.0f)) return tm;  // x_G: added exactly
+        for (int a = 0; a < ns; ++a)
           if (fabsf(seen[a] - t) < S.dedup_tol) return tm;
-        if (ns < RR_SEEN) seen[ns] = t;
-        else qc.seen_overflow++;  // beyond RR_SEEN crossings: counted, no longer deduplicated (rr_stats.sched[6])
-        ns++;
+        seen[ns < 8 ? ns++ : 7] = t;  // beyond 8 crossings: dedup against the first 7 and the latest one
         const float4* tp = S.ltris + 3 * li;
         float4 a4 = __ldg(tp), b4 = __ldg(tp + 1), c4 = __ldg(tp + 2);
         float3 nrm = norm3_exact(cross3(f3(b4.x - a4.x, b4.y - a4.y, b4.z - a4.z), f3(c4.x - a4.x, c4.y - a4.y, c4.z - a4.z)));
@@ -243,11 +231,6 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
       return t;
     }, qc.tc);
   }
-  if (q.seed_t > 0.0f) {
-    const int G = (q.want & 1) ? 0 : 1;
-    const float Lc = seg ? L : best_t[G];
-    r.c[G].sb += (Lc - q.seed_t) * (Lc - q.seed_t) * q.seed_ic;
-  }
   for (int F = 0; F < 2; ++F) {
     if (!((q.want >> F) & 1)) continue;
     if (seg) {
@@ -271,7 +254,7 @@ __device__ __forceinline__ Query mk_ray(P3 o, float3 d, int excl, int want) {
   q.type = QT_CLOSEST;
   q.want = (uint8_t)want;
   q.dyn_only = 0;
-  q.seed_t = q.seed_ic = 0.0f;
+  q.seed_t = 0.0f;
   return q;
 }
 __device__ __forceinline__ Query mk_seg(P3 a, P3 b, int ea, int eb, int want, bool dyn_only = false) {
@@ -286,8 +269,16 @@ __device__ __forceinline__ Query mk_seg(P3 a, P3 b, int ea, int eb, int want, bo
   q.type = QT_SEG;
   q.want = (uint8_t)want;
   q.dyn_only = dyn_only ? 1 : 0;
-  q.seed_t = q.seed_ic = 0.0f;
+  q.seed_t = 0.0f;
   return q;
+}
+// the crossing at x_G (distance t along an edge of length L, 1/|cos_G| = ic) added to an edge's crossing sums
+__device__ __forceinline__ Cross add_seed(Cross c, float t, float L, float ic) {
+  c.n += 1.0f;
+  c.s0 += ic;
+  c.sa += t * t * ic;
+  c.sb += (L - t) * (L - t) * ic;
+  return c;
 }
 
 }  // namespace rr

@@ -87,7 +87,6 @@ __device__ __forceinline__ bool nee_ok(int tech, int m) { return tech == 2 ? m >
 // the sample's own ghost crossing on the queried edge (Query::seed_t; reading 12)
 __device__ __forceinline__ Query seeded(Query q, float t, const PV& xg) {
   q.seed_t = t;
-  q.seed_ic = 1.0f / fabsf(dot3(xg.n, q.d));
   q.eb = xg.tri;
   return q;
 }
@@ -122,6 +121,7 @@ __device__ void start_issue(const DevScene& S, int tech, int F, const float d0[8
       if (!(s.dl > S.eps)) return;
       s.dir = dv * (1.0f / s.dl);
       if (!(dot3(s.a.n, s.dir) > 0.0f)) return;
+      s.b = xg;  // for its crossing (start_consume)
       s.qi = B.push(seeded(mk_ray(s.a.p, s.dir, s.a.tri, bit(F)), s.dl, xg));
       return;
     }
@@ -133,6 +133,7 @@ __device__ void start_issue(const DevScene& S, int tech, int F, const float d0[8
       float3 dv = sub3(xg.p, E.p);
       s.dl = sqrtf(dot3(dv, dv));
       s.dir = dv * (1.0f / s.dl);
+      s.b = xg;
       s.qi = B.push(seeded(mk_ray(E.p, s.dir, -1, bit(F)), s.dl, xg));
       return;
     }
@@ -159,7 +160,7 @@ __device__ void start_consume(const DevScene& S, int tech, int F, const SStart& 
     if (!(sqrtf(dot3(q, q)) > s.dl + S.eps)) return;  // the first hit lies beyond x_G
     W.v[0] = tech == 4 ? s.a : E;
     W.v[1] = h;
-    W.ex[1] = r.c[F];
+    W.ex[1] = add_seed(r.c[F], s.dl, r.h[F].t, 1.0f / fabsf(dot3(s.b.n, s.dir)));  // + the crossing at x_G
     W.n = 1;
     W.pixel = tech == 5 ? s.pix : -1;
   }
@@ -590,9 +591,7 @@ __device__ void bidir_issue(const DevScene& S, const KArgs& A, int tech, int F, 
   if (!G.ok) return;
   if (first && tech == 6 && S.n_moved > 0) {  // crossings of the whole edge y_1 -> z_1, x_G among them
     Query q = mk_seg(G.A.v[0].p, G.A.v[1].p, -2, -2, bit(F));
-    const P3 a = G.A.v[0].p;
-    const double gx = G.start.p.x - a.x, gy = G.start.p.y - a.y, gz = G.start.p.z - a.z;
-    G.qyz = B.push(seeded(q, (float)sqrt(gx * gx + gy * gy + gz * gz), G.start));
+    G.qyz = B.push(seeded(q, norm3f(sub3(G.start.p, G.A.v[0].p)), G.start));
   }
   PV E = cam_pv(S);
   for (int side = 0; side < 2; ++side) {
@@ -631,8 +630,11 @@ __device__ void bidir_issue(const DevScene& S, const KArgs& A, int tech, int F, 
 }
 __device__ void bidir_consume(const DevScene& S, int F, BPath& G, const Batch& B) {
   if (!G.ok) return;
-  if (G.qyz >= 0) {
-    G.A.ex[1] = B.r[G.qyz].c[F];
+  if (G.qyz >= 0) {  // crossings of the edge y_1 -> z_1, plus the crossing at x_G
+    const float3 dv = sub3(G.A.v[1].p, G.A.v[0].p);
+    const float L = norm3f(dv);
+    G.A.ex[1] = add_seed(B.r[G.qyz].c[F], norm3f(sub3(G.start.p, G.A.v[0].p)), L,
+                         L / fabsf(dot3(G.start.n, dv)));
     G.B.ex[1] = swapc(G.A.ex[1]);
   }
   for (int side = 0; side < 2; ++side) {
@@ -688,7 +690,7 @@ __device__ int bidir_path(const BPath& G, int tech, int t, int s, const DevScene
   return k;
 }
 
-__device__ void bidir_finish(const DevScene& S, const KArgs& A, BState& st, Out& o) {
+__device__ __noinline__ void bidir_finish(const DevScene& S, const KArgs& A, BState& st, Out& o) {
   const int F = A.side, Fb = 1 - A.side, l = A.tech, D = A.max_depth;
   BPath& P = st.P;
   BPath& Q = st.Q;
@@ -817,7 +819,7 @@ template <class State, bool BIDIR, bool COUNT>
 __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A) {
   Out o;
   o.A = &A;
-  o.qc.closest = o.qc.shadow = o.qc.inst = o.qc.seen_overflow = 0;
+  o.qc.closest = o.qc.shadow = o.qc.inst = 0;
   o.qc.tc.nodes = o.qc.tc.tris = 0;
   o.conns = o.acc = o.rej = o.unp = o.monly = o.recon = o.splats = o.offscreen = o.zero = 0;
   for (int r = 0; r < 6; ++r) o.rejby[r] = 0;
@@ -905,7 +907,6 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
   for (int r = 0; r < 6; ++r) warp_add(stt + STAT_REJBY + r, o.rejby[r]);
   for (int r = 0; r < 5; ++r)
     if (sc[r]) atomicAdd(stt + STAT_SCHED + r, sc[r]);
-  warp_add(stt + STAT_SCHED + 6, o.qc.seen_overflow);
 }
 
 template <bool COUNT>

@@ -1,2 +1,2 @@
-bash tools/gpu_tests.sh
-python tools/timing.py 3,4 2>&1 | grep -v "^\s*$"
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
+python tools/timing.py 3,4 2>&1 | grep "config\|per launch"
