@@ -154,6 +154,8 @@ typedef struct {
                               rounds, [2] sample steps, [3] queries per round summed, [4] lanes holding
                               a sample summed over rounds, [5] deepest BVH root-to-leaf path in inner
                               nodes (scene property; upload fails above RR_STACK = 64), ([1], [6..7] reserved, 0) */
+  uint64_t r_hist[16];     /* accepted connections of reconnected pairs (R != 1, C7) by floor(log2 R) + 8, clamped to
+                              [0, 15]: bin b holds R in [2^(b-8), 2^(b-7)) (SURVEY 8(f) row 3, R statistics) */
 } rr_stats;
 
 /* one record per emitted base connection (C10), for parity tests */

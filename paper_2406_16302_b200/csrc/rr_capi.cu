@@ -851,6 +851,7 @@ rr_status rr_get_stats(rr_ctx* c, rr_stats* out) {
   out->tris_tested = h[STAT_TRIS];
   for (int r = 0; r < 6; ++r) out->rejected_by[r] = h[STAT_REJBY + r];
   for (int r = 0; r < 8; ++r) out->sched[r] = h[STAT_SCHED + r];
+  for (int r = 0; r < 16; ++r) out->r_hist[r] = h[STAT_RHIST + r];
   out->sched[5] = (uint64_t)c->bvh_depth;
   out->effective_mask = c->last_mask;
   out->n_moved = 0;

@@ -11,7 +11,8 @@ namespace rr {
 enum {
   STAT_SAMPLES = 0, STAT_CONNECTIONS, STAT_ACCEPTED, STAT_REJECTED, STAT_UNPAIRED, STAT_MAPPED_ONLY,
   STAT_RECONNECTED, STAT_CLOSEST, STAT_SHADOW, STAT_INST, STAT_SPLATS, STAT_OFFSCREEN, STAT_ZERO,
-  STAT_NODES, STAT_TRIS, STAT_REJBY, STAT_SCHED = STAT_REJBY + 6, STAT_COUNT = STAT_SCHED + 8
+  STAT_NODES, STAT_TRIS, STAT_REJBY, STAT_SCHED = STAT_REJBY + 6, STAT_RHIST = STAT_SCHED + 8,
+  STAT_COUNT = STAT_RHIST + 16
 };
 
 struct KArgs {

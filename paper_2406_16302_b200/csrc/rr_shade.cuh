@@ -200,7 +200,10 @@ __device__ __forceinline__ void splat(Out& o, int pix, float3 t) {
 __device__ inline void emit_record(Out& o, uint64_t i, int kind, int a, int b, int status, int reason, int pix_p, float3 tp,
                             int pix_q, float3 tq, float R) {
   const KArgs& A = *o.A;
-  if (status == ST_ACCEPTED) o.acc++;
+  if (status == ST_ACCEPTED) {
+    o.acc++;
+    if (R != 1.0f) atomicAdd(A.stats + STAT_RHIST + min(max(ilogbf(R) + 8, 0), 15), 1ull);  // R histogram (rare)
+  }
   else if (status == ST_REJECTED) { o.rej++; o.rejby[reason < 6 ? reason : 0]++; }
   else if (status == ST_UNPAIRED) o.unp++;
   else o.monly++;

@@ -58,12 +58,13 @@ class rr_stats(C.Structure):
                                           "instance_queries", "splats", "offscreen", "zero_pairs",
                                           "nodes_visited", "tris_tested")] + \
                [("rejected_by", C.c_uint64 * 8), ("effective_mask", C.c_uint32), ("n_moved", C.c_uint32),
-                ("sched", C.c_uint64 * 8)]
+                ("sched", C.c_uint64 * 8), ("r_hist", C.c_uint64 * 16)]
 
     def as_dict(self):
-        d = {n: int(getattr(self, n)) for n, _ in self._fields_ if n not in ("rejected_by", "sched")}
+        d = {n: int(getattr(self, n)) for n, _ in self._fields_ if n not in ("rejected_by", "sched", "r_hist")}
         d["rejected_by"] = [int(x) for x in self.rejected_by]
         d["sched"] = [int(x) for x in self.sched]
+        d["r_hist"] = [int(x) for x in self.r_hist]
         return d
 
 

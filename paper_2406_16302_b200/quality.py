@@ -13,7 +13,7 @@ ablations of the method:
   * "residual_vndf"    -- the paper's mode with GGX visible-normal sampling (RR_VNDF).
 
 The reference is NOT any of these estimators: it is the GPU primal renderer (unidirectional NEE/BSDF-MIS path
-tracing, rr_primal.cu, pinned to the oracle's primal renderer) run in both states with the SAME random numbers
+tracing, rr_primal.cu, checked against the CPU reference's primal renderer by the tests) run in both states with the SAME random numbers
 (RR_PRIMAL_SHARED_STREAMS) at high spp -- a correlated, unbiased estimate of I(new) - I(old) that shares no code
 with the residual estimator.  Its own variance is estimated from its chunks and subtracted from every MSE
 (mse = mean |x - ref|^2 - var(ref)), so a reference noisier than intended cannot flatter or hurt an estimator.

@@ -246,6 +246,17 @@ def test_stats_accounting_matches_oracle(torch_cuda):
     # reading 11).  Same rejections, same contributions.
     assert close(g[1] + g[2], by[1] + by[2]), (g, by)
     assert g[2] >= by[2] - 2 and g[1] <= by[1] + 2, (g, by)
+    # the R histogram: accepted connections of reconnected pairs by floor(log2 R)
+    hist = [0] * 16
+    for l in range(1, 8):
+        if (mask >> (l - 1)) & 1:
+            for s in (0, 1):
+                for rec in o.residual(w.args, l, s, 0, o.sample_range(w.args), records=True)[1]:
+                    if rec.status == 0 and rec.R != 1.0:
+                        hist[min(max(math.frexp(rec.R)[1] - 1 + 8, 0), 15)] += 1
+    assert sum(hist) > 100 and sum(st["r_hist"]) > 100
+    for b in range(16):
+        assert abs(st["r_hist"][b] - hist[b]) <= max(3, 5e-3 * hist[b]), (b, st["r_hist"], hist)
 
 
 def test_records_config1_deep(torch_cuda):

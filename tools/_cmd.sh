@@ -1,2 +1,2 @@
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-python tools/timing.py 3,4 2>&1 | grep "config\|per launch"
+bash tools/gpu_tests.sh
+timeout 1500 python tools/quality_r2.py gpurun_out/quality_r2.json > gpurun_out/quality_r2.log 2>&1; echo "quality exit $?"; tail -30 gpurun_out/quality_r2.log
