@@ -253,6 +253,8 @@ struct Scene {
   std::vector<int> has_mat;
   std::vector<Mat> emat[2];
   bool vndf = false;                // render option RR_VNDF (flags bit 32) of the current residual call
+  bool t6_light = false;            // render option RR_T6_TOWARD_LIGHT (flags bit 512)
+  std::vector<V3> emit_centroid;    // area-weighted centroid of each emitter object (world)
   // derived
   double diag, eps;
   V3 cf, cr, cu;  // camera basis
@@ -695,6 +697,17 @@ struct Ctx {
   std::vector<double>* recon_out = nullptr;  // test export: geometry of accepted reconnections (orc_reconnections)
 };
 
+// T6's direction density p_dir(d | x_G) (technique (6) "a direction uniformly toward the light").
+// Default (C12 #9): uniform on the sphere, 1/(4 pi).  RR_T6_TOWARD_LIGHT: an emitter object e is chosen
+// uniformly and d is uniform on the hemisphere facing its centroid c_e, so the density of d is the mixture
+// (1/n_e) sum_e [d . (c_e - x_G) > 0] / (2 pi); +d is the emitter side.
+double t6_pdir(const Scene& S, V3 xg, V3 d) {
+  if (!S.t6_light) return 1.0 / (4.0 * PI);
+  int n = 0;
+  for (const V3& c : S.emit_centroid) n += dot(d, c - xg) > 0 ? 1 : 0;
+  return (double)n / ((double)S.emit_centroid.size() * 2.0 * PI);
+}
+
 Eval eval_path(Ctx& cx, int F, const Path& P, bool check_walk_vis = true, const SeedCrossing* seed = nullptr) {
   const Scene& S = *cx.S;
   Eval ev;
@@ -798,7 +811,7 @@ Eval eval_path(Ctx& cx, int F, const Path& P, bool check_walk_vis = true, const 
         double d2 = dot(d, d);
         V3 w = d * (1.0 / std::sqrt(d2));
         double gg = std::fabs(dot(x[i].n, w)) * std::fabs(dot(x[i + 1].n, w)) / std::fabs(dot(g.n, w)) *
-                    (1.0 / (4.0 * PI)) / d2;
+                    t6_pdir(S, g.p, w) / d2;
         p *= pA_G * gg;
         for (int m = i + 2; m <= k - 2; ++m) p *= fwd[m];
         p *= pL;
@@ -1003,9 +1016,18 @@ Gen generate(Ctx& cx, int tech, int F, const Stream& st, int D) {
     case 6: {  // ghost two ends: full-sphere direction, p_dir = 1/(4 pi)
       if (S.moved_set.tris.empty()) return g;
       Vtx xg = sample_set(S, S.moved_set, 1 - F, d0[0], d0[1], d0[2]);
-      double z = 1.0 - 2.0 * d0[3];
-      double rr = std::sqrt(std::max(0.0, 1.0 - z * z)), phi = 2.0 * PI * d0[4];
-      V3 dir = v3(rr * std::cos(phi), rr * std::sin(phi), z);
+      V3 dir;
+      if (!S.t6_light) {  // uniform sphere: z = 1 - 2 u
+        double z = 1.0 - 2.0 * d0[3];
+        double rr = std::sqrt(std::max(0.0, 1.0 - z * z)), phi = 2.0 * PI * d0[4];
+        dir = v3(rr * std::cos(phi), rr * std::sin(phi), z);
+      } else {  // toward the light: emitter e from d5, d uniform on the hemisphere about c_e - x_G (z = u)
+        int ne = (int)S.emit_centroid.size();
+        int e = std::min((int)std::floor(d0[5] * ne), ne - 1);
+        V3 ax = normalize(S.emit_centroid[e] - xg.p);
+        double z = d0[3], rr = std::sqrt(std::max(0.0, 1.0 - z * z)), phi = 2.0 * PI * d0[4];
+        dir = normalize(local_to_world(ax, rr * std::cos(phi), rr * std::sin(phi), z));
+      }
       if (D < 3) return g;
       Hit hy = closest(S, F, xg.p, dir, -1, &cx.C);
       if (!hy.ok) return g;
@@ -1014,7 +1036,7 @@ Gen generate(Ctx& cx, int tech, int F, const Stream& st, int D) {
       g.ok = true;
       g.start = xg;
       // (x_G, d) -> (z_1, y_1): p_A(x_G) p_dir |n_y.d| |n_z.d| / (|n_G.d| |y_1 - z_1|^2), |y_1 - z_1| = t_y + t_z
-      g.pdf0 = (1.0 / S.moved_set.area) * (1.0 / (4.0 * PI)) * std::fabs(dot(hy.tri->n, dir)) *
+      g.pdf0 = (1.0 / S.moved_set.area) * t6_pdir(S, xg.p, dir) * std::fabs(dot(hy.tri->n, dir)) *
                std::fabs(dot(hz.tri->n, dir)) / (std::fabs(dot(xg.n, dir)) * (hy.t + hz.t) * (hy.t + hz.t));
       g.A.pA = g.B.pA = {0.0, 1.0};
       Vtx y1 = vtx_of_hit(xg.p, dir, hy), z1 = vtx_of_hit(xg.p, dir * -1.0, hz);
@@ -1224,7 +1246,8 @@ typedef struct {
   uint32_t technique_mask;
   uint32_t flags;  // 1 TWO_WAY, 2 RECONNECT, 4 REJECT_MULTI, 32 VNDF (GGX visible-normal sampling),
                    // 64 DIAG_ONE_WAY_ABLATION (one-way with the two-way pairing rules; deliberately biased),
-                   // 256 NO_PATH_MAPPING (two-way sampling, no mapped paths, static paths rejected)
+                   // 256 NO_PATH_MAPPING (two-way sampling, no mapped paths, static paths rejected),
+                   // 512 T6_TOWARD_LIGHT (T6 directions on the hemisphere toward an emitter)
   double jacobian_max, alpha_min, dmin_rel;
 } orc_args;
 
@@ -1773,6 +1796,17 @@ bool load_scene(Oracle& O, const orc_input* in) {
   if (!S.edited_set.tris.empty()) build_set(S, S.edited_set);
   if (!S.moved_set.tris.empty()) build_set(S, S.moved_set);
   if (S.emitters.empty()) { O.err = "scene has no emitter"; return false; }
+  for (const Scene::TriSet& ts : S.emitters) {  // axes of T6's "toward the light" hemispheres
+    V3 c = v3(0, 0, 0);
+    double a = 0;
+    for (int k : ts.tris) {
+      Tri t = make_tri(S, k, 0);
+      double ak = 0.5 * len(cross(t.v1 - t.v0, t.v2 - t.v0));
+      c = c + (t.v0 + t.v1 + t.v2) * (ak / 3.0);
+      a += ak;
+    }
+    S.emit_centroid.push_back(c * (1.0 / a));
+  }
   return true;
 }
 
@@ -1806,6 +1840,7 @@ int orc_residual(void* h, const orc_args* A, int tech, int side, uint64_t i0, ui
                  orc_record* recs, int64_t cap, int64_t* n_recs, orc_stats* stats) {
   Oracle* O = (Oracle*)h;
   O->S.vndf = (A->flags & 32u) != 0;
+  O->S.t6_light = (A->flags & 512u) != 0;
   Ctx cx;
   cx.S = &O->S;
   cx.mask = effective_mask(O->S, A->technique_mask);
@@ -1834,6 +1869,7 @@ int orc_primal_streams(void* h, int F, int stream_state, uint64_t seed, int D, u
                        orc_stats* stats) {
   Oracle* O = (Oracle*)h;
   O->S.vndf = false;  // the primal renderer samples GGX from D(h) |n.h|
+  O->S.t6_light = false;
   Ctx cx;
   cx.S = &O->S;
   cx.mask = 0x7F;
@@ -1857,6 +1893,7 @@ int64_t orc_pdf_check(void* h, const orc_args* A, int tech, int side, uint64_t i
                       int64_t cap) {
   Oracle* O = (Oracle*)h;
   O->S.vndf = (A->flags & 32u) != 0;
+  O->S.t6_light = (A->flags & 512u) != 0;
   const Scene& S = O->S;
   Ctx cx;
   cx.S = &S;
@@ -1899,6 +1936,7 @@ int64_t orc_reconnections(void* h, const orc_args* A, int tech, int side, uint64
                           int64_t cap) {
   Oracle* O = (Oracle*)h;
   O->S.vndf = (A->flags & 32u) != 0;
+  O->S.t6_light = (A->flags & 512u) != 0;
   Ctx cx;
   cx.S = &O->S;
   cx.mask = effective_mask(O->S, A->technique_mask);
@@ -1923,6 +1961,7 @@ void orc_t3_light_dir(const double n[3], double u3, double u4, double out[4]) {
 void orc_debug_sample(void* h, const orc_args* A, int tech, int side, uint64_t i) {
   Oracle* O = (Oracle*)h;
   O->S.vndf = (A->flags & 32u) != 0;
+  O->S.t6_light = (A->flags & 512u) != 0;
   Ctx cx;
   cx.S = &O->S;
   cx.mask = effective_mask(O->S, A->technique_mask);

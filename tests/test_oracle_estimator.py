@@ -152,6 +152,9 @@ def test_masks_l_plus_7_agree_with_7(cfg, D):
             _agree(ref, other)
         full = np.stack(p.map(_render, [(cfg_, 12, s, 0x7F, S.PAPER_FLAGS, D) for s in seeds]))
         _agree(ref, full)
+        # T6 "uniformly toward the light": a variance-only change
+        t6l = np.stack(p.map(_render, [(cfg_, 12, s, 0x60, S.TWO_WAY | S.T6_TOWARD_LIGHT, D) for s in seeds]))
+        _agree(ref, t6l)
 
 
 def test_material_edit_masks_agree():

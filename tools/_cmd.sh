@@ -1,2 +1,4 @@
-bash tools/gpu_tests.sh
-timeout 1500 python tools/quality_r2.py gpurun_out/quality_r2.json > gpurun_out/quality_r2.log 2>&1; echo "quality exit $?"; tail -30 gpurun_out/quality_r2.log
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
+timeout 900 python -m pytest tests -m gpu -q -k "stats_accounting or records_config1_full" > gpurun_out/pt.log 2>&1; echo "pytest $?"; tail -3 gpurun_out/pt.log
+python tools/timing.py 4 2>&1 | grep "config\|per launch"
+python tools/zero_samples.py 4 2>&1 | tail -14
