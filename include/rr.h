@@ -109,6 +109,11 @@ enum {
                               no mapped path -- each base connection splats 2 sigma_F v_F(p) / spp, and a path with
                               no vertex on an edited object and no ghost crossing in its own state (a static path,
                               equal in both states) is rejected.  Unbiased; the ablation of path mapping */
+  RR_T6_TOWARD_LIGHT = 512u, /* T6 samples its direction "uniformly toward the light": an emitter
+                              object e is chosen uniformly (slot-0 d5) and d is uniform on the hemisphere facing e's
+                              area-weighted centroid, +d the emitter side; every T6 candidate pdf uses the mixture
+                              density (1/n_e) sum_e [d.(c_e - x_G) > 0] / (2 pi).  A variance-only variant (SURVEY
+                              8(f) row 4), compiled as its own kernel instantiation; exclusive with RR_VNDF */
   RR_DIAG_ONE_WAY_ABLATION = 64u /* DIAGNOSTIC, deliberately biased: one-way
                               (side N only, N_pix*spp samples per technique, RR_TWO_WAY must be off) but with the
                               two-way pairing rules (RR_RECONNECT / RR_REJECT_MULTI allowed); accepted pairs splat

@@ -41,6 +41,8 @@ struct rr_ctx {
   DevBuf<uint32_t> d_tri_obj, obj_flags, mat_type, mat_type_vndf, obj_mat0, obj_mat1, emit_tris, edited_tris, moved_tris;
   DevBuf<int> d_obj_inst, obj_emitter, emit_off, emit_cnt;
   DevBuf<float> emit_pL, emit_cdf, edited_cdf, moved_cdf;
+  DevBuf<float4> emit_centroid;      // RR_T6_TOWARD_LIGHT: area-weighted centroid of each emitter (world, set_edit)
+  std::vector<std::vector<uint32_t>> emit_tris_host;
   DevBuf<unsigned long long> stats, work;
   DevScene S;
   uint32_t last_mask = 0;
@@ -280,6 +282,7 @@ rr_status rr_scene_upload(rr_ctx* c, const rr_scene_desc* d) {
       eall.insert(eall.end(), etris[e].begin(), etris[e].end());
       ecdf.insert(ecdf.end(), cd.begin(), cd.end());
     }
+    c->emit_tris_host = etris;
     c->emit_off.upload(eoff.data(), ne);
     c->emit_cnt.upload(ecnt.data(), ne);
     c->emit_pL.upload(epl.data(), ne);
@@ -607,6 +610,37 @@ rr_status rr_set_edit(rr_ctx* c, uint32_t n, const rr_edit* edits) {
         mats.push_back(e.new_material);
       }
     }
+    {  // emitter centroids in world space (emitters never move; a material-edited emitter sits at its M_N)
+      const size_t ne = c->emit_tris_host.size();
+      std::vector<float4> cen(ne);
+      for (size_t e = 0; e < ne; ++e) {
+        double cx = 0, cy = 0, cz = 0, at = 0;
+        for (uint32_t t : c->emit_tris_host[e]) {
+          double v[3][3];
+          const int ik = c->obj_inst[c->tri_obj[t]];
+          for (int a = 0; a < 3; ++a) {
+            const float* p = &c->pos[3 * c->idx[3 * t + a]];
+            for (int q = 0; q < 3; ++q) v[a][q] = p[q];
+            if (ik >= 0) {
+              const float* m = S.inst[ik].M[0];
+              double w[3];
+              for (int q = 0; q < 3; ++q) w[q] = m[4 * q] * v[a][0] + m[4 * q + 1] * v[a][1] + m[4 * q + 2] * v[a][2] + m[4 * q + 3];
+              for (int q = 0; q < 3; ++q) v[a][q] = w[q];
+            }
+          }
+          double e1[3], e2[3];
+          for (int q = 0; q < 3; ++q) { e1[q] = v[1][q] - v[0][q]; e2[q] = v[2][q] - v[0][q]; }
+          double nx = e1[1] * e2[2] - e1[2] * e2[1], ny = e1[2] * e2[0] - e1[0] * e2[2], nz = e1[0] * e2[1] - e1[1] * e2[0];
+          double ak = 0.5 * std::sqrt(nx * nx + ny * ny + nz * nz);
+          cx += ak * (v[0][0] + v[1][0] + v[2][0]) / 3.0;
+          cy += ak * (v[0][1] + v[1][1] + v[2][1]) / 3.0;
+          cz += ak * (v[0][2] + v[1][2] + v[2][2]) / 3.0;
+          at += ak;
+        }
+        cen[e] = make_float4((float)(cx / at), (float)(cy / at), (float)(cz / at), 0.0f);
+      }
+      c->emit_centroid.upload_reuse(cen.data(), ne);
+    }
     int n_moved = 0;
     std::vector<uint32_t> moved_tris;
     for (int k = 0; k < ND; ++k) {
@@ -699,8 +733,10 @@ static rr_status check_args(rr_ctx* c, const rr_render_args* a) {
   if ((a->flags & RR_NO_PATH_MAPPING) &&
       (!(a->flags & RR_TWO_WAY) || (a->flags & (RR_RECONNECT | RR_REJECT_MULTI | RR_DIAG_ONE_WAY_ABLATION))))
     return fail(c, RR_E_INVALID, "RR_NO_PATH_MAPPING needs RR_TWO_WAY without RR_RECONNECT / RR_REJECT_MULTI");
+  if ((a->flags & RR_VNDF) && (a->flags & RR_T6_TOWARD_LIGHT))
+    return fail(c, RR_E_INVALID, "RR_VNDF and RR_T6_TOWARD_LIGHT are separate kernel variants; choose one");
   if (a->flags & ~(RR_TWO_WAY | RR_RECONNECT | RR_REJECT_MULTI | RR_ACCUMULATE | RR_COUNT_TRAVERSAL | RR_VNDF |
-                   RR_DIAG_ONE_WAY_ABLATION | RR_NO_PATH_MAPPING))
+                   RR_DIAG_ONE_WAY_ABLATION | RR_NO_PATH_MAPPING | RR_T6_TOWARD_LIGHT))
     return fail(c, RR_E_INVALID, "unknown flag bits");
   if (a->shard_count == 0 || a->shard_index >= a->shard_count) return fail(c, RR_E_INVALID, "bad shard");
   return RR_OK;
@@ -733,6 +769,8 @@ static KArgs make_kargs(rr_ctx* c, const rr_render_args* a, uint32_t mask, int l
   if (K.nopm) K.mask |= 0x100u;  // path_value: static paths rejected
   K.count = (a->flags & RR_COUNT_TRAVERSAL) ? 1 : 0;
   K.mat_type_vndf = (a->flags & RR_VNDF) ? c->mat_type_vndf.p : nullptr;
+  K.t6_centroid = (a->flags & RR_T6_TOWARD_LIGHT) ? c->emit_centroid.p : nullptr;
+  K.n_centroid = (int)c->emit_centroid.n;
   K.reconnect = (a->flags & RR_RECONNECT) ? 1 : 0;
   K.reject_multi = (a->flags & RR_REJECT_MULTI) ? 1 : 0;
   K.seed = a->seed;

@@ -32,7 +32,8 @@ struct __align__(16) Query {
   float tmax;            // QT_SEG: segment length L; QT_CLOSEST: unused
   int ea, eb;            // excluded triangles (origin, end)
   uint8_t type, want;    // want: bit F set -> evaluate state F
-  uint8_t dyn_only, pad;
+  uint8_t dyn_only;
+  uint8_t rev;           // RR_T6_TOWARD_LIGHT kernels: the path runs this edge against the query's direction
   // x_G of a T4 / T5 / T6 sample on this ray / segment (reading 12): seed_t > 0 its distance, eb its
   // ghost triangle.  The ghost-crossing jobs skip that crossing (a hit of triangle eb, or within dedup_tol of
   // seed_t); the consumer adds it exactly (add_seed), so it counts once whether or not the non-watertight
@@ -137,8 +138,25 @@ __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay
 // COUNT: count node fetches and triangle tests (rr_stats.nodes_visited / tris_tested; off in timed renders,
 // where the two counters cost ~3%).  Inlined into its call site: under the 32-register budget a call boundary
 // forces the scene pointers through generic loads and spills (-9% on config 4 when inlined).
+#if defined(RR_T6L_KERNELS) && RR_T6L_KERNELS
+// RR_T6_TOWARD_LIGHT: 4 pi p_dir(d | x) of T6's direction d at a ghost point x (the oracle's t6_pdir):
+// (2 / n_e) #{e : d . (c_e - x) > 0}; 1 for the uniform sphere
+__device__ __forceinline__ float t6_pdir4pi(const float4* c, int n, float3 x, float3 d) {
+  int k = 0;
+  for (int e = 0; e < n; ++e) {
+    const float4 ce = __ldg(c + e);
+    k += dot3(d, f3(ce.x - x.x, ce.y - x.y, ce.z - x.z)) > 0.0f ? 1 : 0;
+  }
+  return 2.0f * (float)k / (float)n;
+}
+#endif
+
 template <bool COUNT>
-__device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRes& r, QCount& qc) {
+__device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRes& r, QCount& qc
+#if defined(RR_T6L_KERNELS) && RR_T6L_KERNELS
+                                          , const float4* t6c, int t6n
+#endif
+) {
   const bool seg = q.type == QT_SEG;
   const float L = q.tmax;
   r.ok[0] = r.ok[1] = 0;
@@ -207,9 +225,16 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
         float4 a4 = __ldg(tp), b4 = __ldg(tp + 1), c4 = __ldg(tp + 2);
         float3 nrm = norm3_exact(cross3(f3(b4.x - a4.x, b4.y - a4.y, b4.z - a4.z), f3(c4.x - a4.x, c4.y - a4.y, c4.z - a4.z)));
         float inv_c = 1.0f / fabsf(dot3(nrm, d));
+#if defined(RR_T6L_KERNELS) && RR_T6L_KERNELS
+        // s0 carries 4 pi p_dir of the path's direction through this crossing (T6's candidate pdf)
+        const float3 xw = q.o + q.d * t;
+        const float pd = t6_pdir4pi(t6c, t6n, xw, q.rev ? q.d * -1.0f : q.d);
+#else
+        const float pd = 1.0f;
+#endif
         Cross& cc = r.c[F];
         cc.n += 1.0f;
-        cc.s0 += inv_c;
+        cc.s0 += inv_c * pd;
         cc.sa += t * t * inv_c;
         cc.sb += (Lc - t) * (Lc - t) * inv_c;
         return tm;
@@ -254,6 +279,9 @@ __device__ __forceinline__ Query mk_ray(P3 o, float3 d, int excl, int want) {
   q.type = QT_CLOSEST;
   q.want = (uint8_t)want;
   q.dyn_only = 0;
+#if defined(RR_T6L_KERNELS) && RR_T6L_KERNELS
+  q.rev = 0;
+#endif
   q.seed_t = 0.0f;
   return q;
 }
@@ -269,6 +297,9 @@ __device__ __forceinline__ Query mk_seg(P3 a, P3 b, int ea, int eb, int want, bo
   q.type = QT_SEG;
   q.want = (uint8_t)want;
   q.dyn_only = dyn_only ? 1 : 0;
+#if defined(RR_T6L_KERNELS) && RR_T6L_KERNELS
+  q.rev = 0;
+#endif
   q.seed_t = 0.0f;
   return q;
 }

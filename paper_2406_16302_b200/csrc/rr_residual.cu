@@ -17,6 +17,9 @@
 #ifndef RR_VNDF_KERNELS
 #define RR_VNDF_KERNELS 0  // 1: this TU is the RR_VNDF instantiation (rr_residual_vndf.cu)
 #endif
+#ifndef RR_T6L_KERNELS
+#define RR_T6L_KERNELS 0  // 1: this TU is the RR_T6_TOWARD_LIGHT instantiation (rr_residual_t6l.cu)
+#endif
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -32,8 +35,20 @@ namespace rr {
 // visible-normal sampling compiled in), so that the default kernels carry no code of the variant
 #if RR_VNDF_KERNELS
 namespace kvndf {
+#elif RR_T6L_KERNELS
+namespace kt6l {
 #else
 namespace kplain {
+#endif
+// RR_T6_TOWARD_LIGHT (kt6l only): the path runs this query's edge against its direction (crossing p_dir)
+#if RR_T6L_KERNELS
+__device__ __forceinline__ Query orient(Query q, bool rev) {
+  q.rev = rev ? 1 : 0;
+  return q;
+}
+#define RR_ORIENT(q, rev) orient(q, rev)
+#else
+#define RR_ORIENT(q, rev) (q)
 #endif
 
 #define NQ 10
@@ -180,8 +195,10 @@ __device__ __forceinline__ void single_issue(const DevScene& S, const KArgs& A, 
   st.hdiv = st.hdiv || vdiff || (hasP != hasQ);
   if (hasP && edited(S, P.v[m].obj)) st.dynP++;
   if (hasQ && edited(S, Q.v[m].obj)) st.dynQ++;
-  if (st.recon == 3) st.q_recon = B.push(mk_seg(Q.v[st.w].p, P.v[st.w + 1].p, Q.v[st.w].tri, P.v[st.w + 1].tri, bit(Fb)));
-  if (st.suffix_pending) st.q_suffix = B.push(mk_seg(P.v[m - 1].p, P.v[m].p, P.v[m - 1].tri, P.v[m].tri, bit(Fb), true));
+  if (st.recon == 3)
+    st.q_recon = B.push(RR_ORIENT(mk_seg(Q.v[st.w].p, P.v[st.w + 1].p, Q.v[st.w].tri, P.v[st.w + 1].tri, bit(Fb)), Lroot));
+  if (st.suffix_pending)
+    st.q_suffix = B.push(RR_ORIENT(mk_seg(P.v[m - 1].p, P.v[m].p, P.v[m - 1].tri, P.v[m].tri, bit(Fb), true), Lroot));
   float d[8];
   st.rng.dims((uint32_t)m, d);
   // ---- connection at m
@@ -241,9 +258,9 @@ __device__ __forceinline__ void single_issue(const DevScene& S, const KArgs& A, 
     st.walk_shared = st.qActive && st.okP && st.okQ && !vdiff && !dirdiv;
     st.attempt = A.reconnect && st.recon == 0 && st.qActive && hasP && st.div_m && rough_enough(mp, A.alpha_min) &&
                  rough_enough(mq, A.alpha_min);
-    if (st.okP) st.q_wp = B.push(mk_ray(P.v[m].p, st.woP, P.v[m].tri, bit(F) | (st.walk_shared ? bit(Fb) : 0)));
+    if (st.okP) st.q_wp = B.push(RR_ORIENT(mk_ray(P.v[m].p, st.woP, P.v[m].tri, bit(F) | (st.walk_shared ? bit(Fb) : 0)), Lroot));
     if (st.qActive && st.okQ && !st.walk_shared && !st.attempt)
-      st.q_wq = B.push(mk_ray(Q.v[m].p, st.woQ, Q.v[m].tri, bit(Fb)));
+      st.q_wq = B.push(RR_ORIENT(mk_ray(Q.v[m].p, st.woQ, Q.v[m].tri, bit(Fb)), Lroot));
   }
 }
 
@@ -551,14 +568,25 @@ __device__ void bidir_start_issue(const DevScene& S, const KArgs& A, int tech, i
     G.dir0 = wl;
     G.dir1 = we;
     G.q0 = B.push(mk_ray(xd.p, wl, xd.tri, bit(F)));
-    G.q1 = B.push(mk_ray(xd.p, we, xd.tri, bit(F)));
+    G.q1 = B.push(RR_ORIENT(mk_ray(xd.p, we, xd.tri, bit(F)), true));  // the sensor side runs against the path
   } else {
     if (S.n_moved == 0 || D < 3) return;
     PV xg = sample_set(S, S.moved_tris, S.moved_cdf, S.n_moved, 1 - F, d0[0], d0[1], d0[2]);
+#if RR_T6L_KERNELS
+    // "uniformly toward the light": emitter e from d5, d uniform on the hemisphere about c_e - x_G
+    const int e = min((int)floorf(d0[5] * (float)A.n_centroid), A.n_centroid - 1);
+    const float4 ce = __ldg(A.t6_centroid + e);
+    const float3 ax = norm3_exact(sub3(make_double3(ce.x, ce.y, ce.z), xg.p));
+    float z = d0[3];
+    float rr = sqrtf(fmaxf(0.0f, 1.0f - z * z)), s, c;
+    sincosf(2.0f * RR_PI_F * d0[4], &s, &c);
+    float3 dir = norm3_exact(to_world(ax, rr * c, rr * s, z));
+#else
     float z = 1.0f - 2.0f * d0[3];
     float rr = 2.0f * sqrtf(d0[3] * (1.0f - d0[3])), s, c;  // sqrt(1 - z^2), no cancellation
     sincosf(2.0f * RR_PI_F * d0[4], &s, &c);
     float3 dir = f3(rr * c, rr * s, z);
+#endif
     G.start = xg;
     G.dir0 = dir;
     G.dir1 = dir * -1.0f;
@@ -591,7 +619,7 @@ __device__ void bidir_issue(const DevScene& S, const KArgs& A, int tech, int F, 
   if (!G.ok) return;
   if (first && tech == 6 && S.n_moved > 0) {  // crossings of the whole edge y_1 -> z_1, x_G among them
     Query q = mk_seg(G.A.v[0].p, G.A.v[1].p, -2, -2, bit(F));
-    G.qyz = B.push(seeded(q, norm3f(sub3(G.start.p, G.A.v[0].p)), G.start));
+    G.qyz = B.push(RR_ORIENT(seeded(q, norm3f(sub3(G.start.p, G.A.v[0].p)), G.start), true));
   }
   PV E = cam_pv(S);
   for (int side = 0; side < 2; ++side) {
@@ -620,7 +648,7 @@ __device__ void bidir_issue(const DevScene& S, const KArgs& A, int tech, int F, 
       rng.dims((uint32_t)((side == 0 ? 0 : 16) + m), d);
       Mat mt = load_mat(S, (uint32_t)W.v[m].obj, F);
       if (bsdf_sample(mt, W.v[m].n, norm3_exact(sub3(W.v[m - 1].p, W.v[m].p)), d[1], d[2], W.wd))
-        W.qw = B.push(mk_ray(W.v[m].p, W.wd, W.v[m].tri, bit(F)));
+        W.qw = B.push(RR_ORIENT(mk_ray(W.v[m].p, W.wd, W.v[m].tri, bit(F)), side == 0));  // side A: against the path
       else
         W.ended = true;
     } else {
@@ -628,13 +656,18 @@ __device__ void bidir_issue(const DevScene& S, const KArgs& A, int tech, int F, 
     }
   }
 }
-__device__ void bidir_consume(const DevScene& S, int F, BPath& G, const Batch& B) {
+__device__ void bidir_consume(const DevScene& S, const KArgs& A, int F, BPath& G, const Batch& B) {
   if (!G.ok) return;
   if (G.qyz >= 0) {  // crossings of the edge y_1 -> z_1, plus the crossing at x_G
     const float3 dv = sub3(G.A.v[1].p, G.A.v[0].p);
     const float L = norm3f(dv);
+#if RR_T6L_KERNELS
+    const float pd = t6_pdir4pi(A.t6_centroid, A.n_centroid, f3of(G.start.p), G.dir0);  // +d: z_1 -> y_1
+#else
+    const float pd = 1.0f;
+#endif
     G.A.ex[1] = add_seed(B.r[G.qyz].c[F], norm3f(sub3(G.start.p, G.A.v[0].p)), L,
-                         L / fabsf(dot3(G.start.n, dv)));
+                         L / fabsf(dot3(G.start.n, dv)) * pd);
     G.B.ex[1] = swapc(G.A.ex[1]);
   }
   for (int side = 0; side < 2; ++side) {
@@ -770,8 +803,8 @@ __device__ bool bidir_step(const DevScene& S, const KArgs& A, BState& st, Batch&
       if (B.n > 0) return true;
       continue;
     }
-    bidir_consume(S, F, st.P, B);
-    bidir_consume(S, Fb, st.Q, B);
+    bidir_consume(S, A, F, st.P, B);
+    bidir_consume(S, A, Fb, st.Q, B);
     B.n = 0;
     bidir_issue(S, A, l, F, st.rng, st.nmax, st.P, B, false);
     bidir_issue(S, A, l, Fb, st.rng, st.nmax, st.Q, B, false);
@@ -878,7 +911,11 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
     }
     sc[4] += active;
     for (int k = 0; k < nmax; ++k)
+#if RR_T6L_KERNELS
+      if (k < B.n) run_query<COUNT>(S, B.q[k], B.r[k], o.qc, A.t6_centroid, A.n_centroid);
+#else
       if (k < B.n) run_query<COUNT>(S, B.q[k], B.r[k], o.qc);
+#endif
     if (active) {
       sc[2]++;
       bool go;
@@ -930,7 +967,11 @@ inline void launch_kernels(const DevScene& S, const KArgs& A, int grid, cudaStre
 }
 }  // namespace kplain / kvndf
 
-#if RR_VNDF_KERNELS
+#if RR_T6L_KERNELS
+void launch_residual_t6l(const DevScene& S, const KArgs& A, int grid, cudaStream_t st) {
+  kt6l::launch_kernels(S, A, grid, st);
+}
+#elif RR_VNDF_KERNELS
 void launch_residual_vndf(const DevScene& S0, const KArgs& A, int grid, cudaStream_t st) {
   DevScene S = S0;
   S.mat_type = A.mat_type_vndf;  // GGX = 2: visible-normal sampling
@@ -1019,7 +1060,8 @@ int residual_grid(bool bidir, uint64_t n) {
 }
 int residual_block() { return RR_BLOCK; }
 void launch_residual(const DevScene& S, const KArgs& A, int grid, cudaStream_t st) {
-  if (A.mat_type_vndf) launch_residual_vndf(S, A, grid, st);  // RR_VNDF: the other instantiation
+  if (A.t6_centroid) launch_residual_t6l(S, A, grid, st);  // RR_T6_TOWARD_LIGHT: its own instantiation
+  else if (A.mat_type_vndf) launch_residual_vndf(S, A, grid, st);  // RR_VNDF: the other instantiation
   else kplain::launch_kernels(S, A, grid, st);
 }
 void launch_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out, cudaStream_t st) {
@@ -1032,5 +1074,5 @@ void launch_segment(const DevScene& S, uint32_t n, const float* segs, float* out
   k_segment<<<(n + 127) / 128, 128, 0, st>>>(S, n, segs, out);
 }
 
-#endif  // RR_VNDF_KERNELS
+#endif  // RR_VNDF_KERNELS / RR_T6L_KERNELS
 }  // namespace rr

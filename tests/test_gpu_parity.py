@@ -314,6 +314,18 @@ def test_records_diag_one_way_config1(torch_cuda):
     record_parity(w, args)
 
 
+@pytest.mark.parametrize("cfg", ["c1", "rev", 3, 4, 5])
+def test_records_t6_toward_light(torch_cuda, cfg):
+    """RR_T6_TOWARD_LIGHT: T6 directions on the hemisphere toward an emitter, and every
+    path's T6 candidate pdf with the mixture direction density (its own kernel instantiation, rr_residual_t6l.cu)."""
+    w = {"c1": S.config1, "rev": lambda: S.occluder_reveal(32, 32, spp=8, max_depth=5)}.get(cfg, lambda: S.load_config(cfg))()
+    args = dataclasses.replace(w.args, flags=S.PAPER_FLAGS | S.T6_TOWARD_LIGHT)
+    if cfg in ("c1", "rev"):
+        record_parity(w, args)
+    else:
+        record_parity(w, args, n_per=1024, strided=True)
+
+
 @pytest.mark.parametrize("cfg", [1, 2, 4])
 def test_records_no_path_mapping(torch_cuda, cfg):
     """RR_NO_PATH_MAPPING ("incremental w/o PM"): every connection unpaired, static paths rejected."""
@@ -475,7 +487,7 @@ def test_invalid_arguments_are_refused(torch_cuda):
     for bad in (dict(technique_mask=0x3F), dict(spp=3), dict(max_depth=0), dict(max_depth=11),
                 dict(flags=S.RECONNECT), dict(layer_mask=0x80), dict(flags=S.PAPER_FLAGS | 512),
                 dict(flags=S.PAPER_FLAGS | S.DIAG_ONE_WAY), dict(flags=S.PAPER_FLAGS | S.NO_PATH_MAPPING),
-                dict(flags=S.NO_PATH_MAPPING)):
+                dict(flags=S.NO_PATH_MAPPING), dict(flags=S.PAPER_FLAGS | S.VNDF | S.T6_TOWARD_LIGHT)):
         with pytest.raises(RRError):
             r.render_residual(dataclasses.replace(w.args, **bad))
     for bad in (dict(state=2), dict(spp=0), dict(max_depth=0), dict(max_depth=11)):
