@@ -1,4 +1,3 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-timeout 900 python -m pytest tests -m gpu -q -k "stats_accounting or records_config1_full" > gpurun_out/pt.log 2>&1; echo "pytest $?"; tail -3 gpurun_out/pt.log
+timeout 1200 python -m pytest tests -m gpu -q -k "t6_toward or invalid or stats_accounting" > gpurun_out/pt.log 2>&1; echo "pytest $?"; tail -5 gpurun_out/pt.log; grep -E "^E .*Assert" gpurun_out/pt.log | cut -c1-400 | head -5
 python tools/timing.py 4 2>&1 | grep "config\|per launch"
-python tools/zero_samples.py 4 2>&1 | tail -14
