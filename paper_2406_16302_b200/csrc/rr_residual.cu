@@ -74,6 +74,26 @@ struct SWalk {
   int n;              // number of walk vertices (0: the technique failed)
   int pixel;          // fixed pixel (T7, T2, T5)
 };
+// the connection path of a single walk read in place (no copy into path arrays): E-rooted (T7 / T2 / T5)
+// (E, v_1..v_m, L) or L-rooted (T1 / T4) (E, v_m..v_1, x_L); cn = the connection edge's crossings as queried
+// (from v_m toward L, or from v_m toward E)
+struct SPathView {
+  const SWalk* W;
+  const PV* E;
+  const PV* L;
+  Cross cn;
+  int m;
+  bool lroot;
+  __device__ __forceinline__ const PV& v(int i) const {
+    if (i == 0) return *E;
+    if (i <= m) return lroot ? W->v[m + 1 - i] : W->v[i];
+    return lroot ? W->v[0] : *L;
+  }
+  __device__ __forceinline__ Cross c(int i) const {
+    if (!lroot) return i < m ? W->ex[i + 1] : cn;
+    return i == 0 ? swapc(cn) : swapc(W->ex[m + 1 - i]);
+  }
+};
 struct SStart {  // start element of one side, kept between issue and consume
   PV a, b;
   float dl;
@@ -297,11 +317,9 @@ __device__ __forceinline__ bool single_consume(const DevScene& S, const KArgs& A
   if (l == 7 && m == 1) {
     bool pe = hasP && __ldg(&S.obj_emitter[P.v[1].obj]) >= 0;
     bool qe = hasQ && __ldg(&S.obj_emitter[Q.v[1].obj]) >= 0;
-    PV x[2];
-    Cross ce[1];
     float3 vp = f3(0.f, 0.f, 0.f), vq = vp;
-    if (pe) { x[0] = E; x[1] = P.v[1]; ce[0] = P.ex[1]; vp = path_value(S, x, ce, 2, F, A.mask); }
-    if (qe) { x[0] = E; x[1] = Q.v[1]; ce[0] = Q.ex[1]; vq = path_value(S, x, ce, 2, Fb, A.mask); }
+    if (pe) vp = path_value_t(S, SPathView{&P, &E, nullptr, cross_zero(), 1, false}, 2, F, A.mask);
+    if (qe) vq = path_value_t(S, SPathView{&Q, &E, nullptr, cross_zero(), 1, false}, 2, Fb, A.mask);
     if (pe) {
       int stt = qe ? ST_ACCEPTED : ST_UNPAIRED;
       if (stt == ST_ACCEPTED && A.reject_multi && st.hdiv && (st.dynP >= 2 || st.dynQ >= 2)) stt = ST_REJECTED;
@@ -314,44 +332,22 @@ __device__ __forceinline__ bool single_consume(const DevScene& S, const KArgs& A
   if (st.has_conn) {
     const bool reconnected_here = (st.recon == 1 && m >= st.w + 1);
     bool qc_ = st.qc_ && !(st.recon == 2 && m >= st.w + 1) && !(reconnected_here && m >= st.reject_from);
-    PV x[RR_MAXV + 1];
-    Cross ce[RR_MAXV + 1];
     float3 vp = f3(0.f, 0.f, 0.f), vq = vp;
     int pixp, pixq;
     if (!Lroot) {
       pixp = P.pixel;
       pixq = Q.pixel;
-      if (st.pc_ && B.r[st.q_cp].ok[F]) {
-        x[0] = E;
-        for (int j = 1; j <= m; ++j) { x[j] = P.v[j]; ce[j - 1] = P.ex[j]; }
-        x[m + 1] = st.L;
-        ce[m] = B.r[st.q_cp].c[F];
-        vp = path_value(S, x, ce, m + 2, F, A.mask);
-      }
-      if (qc_ && B.r[st.q_cq].ok[Fb]) {
-        x[0] = E;
-        for (int j = 1; j <= m; ++j) { x[j] = Q.v[j]; ce[j - 1] = Q.ex[j]; }
-        x[m + 1] = st.L;
-        ce[m] = B.r[st.q_cq].c[Fb];
-        vq = path_value(S, x, ce, m + 2, Fb, A.mask);
-      }
+      if (st.pc_ && B.r[st.q_cp].ok[F])
+        vp = path_value_t(S, SPathView{&P, &E, &st.L, B.r[st.q_cp].c[F], m, false}, m + 2, F, A.mask);
+      if (qc_ && B.r[st.q_cq].ok[Fb])
+        vq = path_value_t(S, SPathView{&Q, &E, &st.L, B.r[st.q_cq].c[Fb], m, false}, m + 2, Fb, A.mask);
     } else {
       pixp = st.pixp;
       pixq = st.pixq;
-      if (st.pc_ && st.q_cp >= 0 && B.r[st.q_cp].ok[F]) {
-        x[0] = E;
-        ce[0] = swapc(B.r[st.q_cp].c[F]);
-        for (int j = 1; j <= m; ++j) { x[j] = P.v[m + 1 - j]; ce[j] = swapc(P.ex[m + 1 - j]); }
-        x[m + 1] = P.v[0];
-        vp = path_value(S, x, ce, m + 2, F, A.mask);
-      }
-      if (qc_ && st.q_cq >= 0 && B.r[st.q_cq].ok[Fb]) {
-        x[0] = E;
-        ce[0] = swapc(B.r[st.q_cq].c[Fb]);
-        for (int j = 1; j <= m; ++j) { x[j] = Q.v[m + 1 - j]; ce[j] = swapc(Q.ex[m + 1 - j]); }
-        x[m + 1] = Q.v[0];
-        vq = path_value(S, x, ce, m + 2, Fb, A.mask);
-      }
+      if (st.pc_ && st.q_cp >= 0 && B.r[st.q_cp].ok[F])
+        vp = path_value_t(S, SPathView{&P, &E, nullptr, B.r[st.q_cp].c[F], m, true}, m + 2, F, A.mask);
+      if (qc_ && st.q_cq >= 0 && B.r[st.q_cq].ok[Fb])
+        vq = path_value_t(S, SPathView{&Q, &E, nullptr, B.r[st.q_cq].c[Fb], m, true}, m + 2, Fb, A.mask);
     }
     const int kind = Lroot ? 2 : 1;
     if (st.pc_) {
@@ -951,7 +947,10 @@ __global__ void __launch_bounds__(RR_BLOCK, RR_MIN_BLOCKS) k_residual_single(con
   residual_loop<SState, false, COUNT>(S, A);
 }
 template <bool COUNT>
-__global__ void __launch_bounds__(RR_BLOCK, RR_MIN_BLOCKS) k_residual_bidir(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
+#ifndef RR_MIN_BLOCKS_BIDIR
+#define RR_MIN_BLOCKS_BIDIR RR_MIN_BLOCKS
+#endif
+__global__ void __launch_bounds__(RR_BLOCK, RR_MIN_BLOCKS_BIDIR) k_residual_bidir(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A) {
   residual_loop<BState, true, COUNT>(S, A);
 }
 

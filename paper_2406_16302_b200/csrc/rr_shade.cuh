@@ -119,40 +119,41 @@ __device__ __forceinline__ float area_pdf(const DevScene& S, int F, const PV& pr
 // Computed as (f / p_T7) / (1 + sum_c p_c / p_T7).  mask bit 8 (RR_NO_PATH_MAPPING): a static path (no vertex
 // on an edited object, no ghost crossing on any edge) has value 0.
 // ------------------------------------------------------------------------------------------------
-__device__ inline float3 path_value(const DevScene& S, const PV* x, const Cross* e, int k, int F, uint32_t mask) {
+template <class Path>
+__device__ inline float3 path_value_t(const DevScene& S, const Path& px, int k, int F, uint32_t mask) {
   const float3 zero = f3(0.f, 0.f, 0.f);
-  float3 d01 = sub3(x[1].p, x[0].p);
+  float3 d01 = sub3(px.v(1).p, px.v(0).p);
   float dd01 = dot3(d01, d01);
   float3 w01 = d01 * (1.0f / sqrtf(dd01));
   float cth = dot3(w01, S.cf);
   if (!(cth > 0.0f)) return zero;
-  const PV& L = x[k - 1];
+  const PV& L = px.v(k - 1);
   float4 le4 = __ldg(&S.obj_emit[L.obj]);
   float3 Le = f3(le4.x, le4.y, le4.z);
-  if (!(dot3(L.n, sub3(x[k - 2].p, L.p)) > 0.0f)) return zero;  // front face only
+  if (!(dot3(L.n, sub3(px.v(k - 2).p, L.p)) > 0.0f)) return zero;  // front face only
   const bool reject_static = (mask & 0x100u) != 0;
-  bool dyn_any = e[0].n > 0.0f;
+  bool dyn_any = px.c(0).n > 0.0f;
   if (k == 2) return (reject_static && !dyn_any) ? zero : Le;  // direct view: W_e G / p_cam = 1, Pi = p_T7
-  float cos1 = fabsf(dot3(x[1].n, w01));
+  float cos1 = fabsf(dot3(px.v(1).n, w01));
   float invpcam = S.Aplane * cth * cth * cth * dd01 / cos1;  // 1 / p_cam(x_1)
   float pL = __ldg(&S.emit_pL[__ldg(&S.obj_emitter[L.obj])]);
   const bool t1 = mask & 1u, t2 = mask & 2u, t3 = mask & 4u, t4 = mask & 8u, t5 = mask & 16u, t6 = mask & 32u;
   float3 T = f3(1.f, 1.f, 1.f);
   float sum = 1.0f;  // T7
-  if (t5 && e[0].n > 0.0f) sum += S.pA_G * S.Aplane * cth * cth * cth * e[0].sa;
+  if (t5 && px.c(0).n > 0.0f) sum += S.pA_G * S.Aplane * cth * cth * cth * px.c(0).sa;
   float Q = 1.0f;  // prod_{m < i} rev_m / fwd_{m+1}
   for (int i = 1; i <= k - 2; ++i) {
-    Mat m = load_mat(S, (uint32_t)x[i].obj, F);
-    float3 wi = norm3_exact(sub3(x[i - 1].p, x[i].p));
-    float3 dv = sub3(x[i + 1].p, x[i].p);
+    Mat m = load_mat(S, (uint32_t)px.v(i).obj, F);
+    float3 wi = norm3_exact(sub3(px.v(i - 1).p, px.v(i).p));
+    float3 dv = sub3(px.v(i + 1).p, px.v(i).p);
     float d2 = dot3(dv, dv);
     float3 wo = dv * (1.0f / sqrtf(d2));
-    float3 rho = bsdf_eval(m, x[i].n, wi, wo);
-    float pf = bsdf_pdf(m, x[i].n, wi, wo);
-    float cout = fabsf(dot3(x[i].n, wo));
-    float cin_next = fabsf(dot3(x[i + 1].n, wo));
-    bool dyn = edited(S, x[i].obj);
-    dyn_any = dyn_any || dyn || e[i].n > 0.0f;
+    float3 rho = bsdf_eval(m, px.v(i).n, wi, wo);
+    float pf = bsdf_pdf(m, px.v(i).n, wi, wo);
+    float cout = fabsf(dot3(px.v(i).n, wo));
+    float cin_next = fabsf(dot3(px.v(i + 1).n, wo));
+    bool dyn = edited(S, px.v(i).obj);
+    dyn_any = dyn_any || dyn || px.c(i).n > 0.0f;
     if (!(pf > 0.0f)) return zero;  // f = 0 (rho = 0 exactly where pf = 0 for these BSDFs)
     if (i < k - 2) {
       T = mul3(T, rho * (cout / pf));
@@ -163,20 +164,31 @@ __device__ inline float3 path_value(const DevScene& S, const PV* x, const Cross*
     if (dyn) {
       if (i == k - 2) { if (t1) sum += base; }                          // T1: adjacent to the emitter
       else if (i == 1) { if (t2) sum += S.pA_D * invpcam; }             // T2: adjacent to the sensor
-      else if (t3) sum += base * (fmaxf(0.0f, dot3(x[i].n, wo)) * RR_INV_PI_F) / pf;  // T3
+      else if (t3) sum += base * (fmaxf(0.0f, dot3(px.v(i).n, wo)) * RR_INV_PI_F) / pf;  // T3
     }
-    if (e[i].n > 0.0f) {
-      if (i + 1 == k - 1) { if (t4) sum += S.pA_G * e[i].sb * cout / d2 * invpcam * Q; }  // T4 (Eq. vertex1pdf)
-      else if (t6) sum += S.pA_G * (0.25f * RR_INV_PI_F) * e[i].s0 * cout / pf * invpcam * Q;  // T6
+    if (px.c(i).n > 0.0f) {
+      if (i + 1 == k - 1) { if (t4) sum += S.pA_G * px.c(i).sb * cout / d2 * invpcam * Q; }  // T4 (Eq. vertex1pdf)
+      else if (t6) sum += S.pA_G * (0.25f * RR_INV_PI_F) * px.c(i).s0 * cout / pf * invpcam * Q;  // T6
     }
     if (i <= k - 3) {  // q_i = rev_i / fwd_{i+1} on edge (i, i+1)
-      Mat mn = load_mat(S, (uint32_t)x[i + 1].obj, F);
-      float pr = bsdf_pdf(mn, x[i + 1].n, norm3_exact(sub3(x[i + 2].p, x[i + 1].p)), wo * -1.0f);
+      Mat mn = load_mat(S, (uint32_t)px.v(i + 1).obj, F);
+      float pr = bsdf_pdf(mn, px.v(i + 1).n, norm3_exact(sub3(px.v(i + 2).p, px.v(i + 1).p)), wo * -1.0f);
       Q *= pr * cout / (pf * cin_next);
     }
   }
   if (reject_static && !dyn_any) return zero;
   return T * (1.0f / sum);
+}
+
+// the connection path as two contiguous arrays x[0..k-1], e[0..k-2]
+struct PathArrays {
+  const PV* x;
+  const Cross* e;
+  __device__ __forceinline__ const PV& v(int i) const { return x[i]; }
+  __device__ __forceinline__ Cross c(int i) const { return e[i]; }
+};
+__device__ inline float3 path_value(const DevScene& S, const PV* x, const Cross* e, int k, int F, uint32_t mask) {
+  return path_value_t(S, PathArrays{x, e}, k, F, mask);
 }
 
 // ------------------------------------------------------------------------------------------------
