@@ -328,7 +328,8 @@ def run_ours(a):
     mrays = (closest + shadow) * a.steps / (ms / 1e3) / 1e6
     # ---- roofline of the dominant kernel: the (technique, both sides) launches with the largest time share.
     # Its algorithmic bytes = 64 B per BVH2 node fetched + 48 B per triangle tested, counted by
-    # the kernels; attributed to the technique by two extra (untimed) renders, {l, T7} minus {T7}.
+    # the kernels in an extra (untimed) render of exactly those launches: the full technique mask (same MIS and
+    # pairing) with layer_mask = that technique.
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         peaks = json.load(open(peaks_path))
@@ -344,17 +345,14 @@ def run_ours(a):
         per_tech_ms[l] = per_tech_ms.get(l, 0.0) + x
     dom = max(per_tech_ms, key=per_tech_ms.get)
 
-    def counts(m):  # untimed render with traversal counting
-        r.render_residual(dataclasses.replace(args, technique_mask=m), image=img, shard_index=rank, shard_count=world,
-                          count_traversal=True)
+    def counts(layer):  # untimed render with traversal counting (layer 0: every launch of the step)
+        r.render_residual(dataclasses.replace(args, layer_mask=layer), image=img, shard_index=rank,
+                          shard_count=world, count_traversal=True)
         q = r.get_stats()
         return q["nodes_visited"], q["tris_tested"]
 
-    nodes, tris = counts(args.technique_mask)  # all launches of the step
-    n7, t7 = counts(0x40)
-    nd, td = (n7, t7) if dom == 7 else counts(0x40 | (1 << (dom - 1)))
-    if dom != 7:
-        nd, td = nd - n7, td - t7
+    nodes, tris = counts(0)
+    nd, td = counts(1 << (dom - 1))
     dom_bytes = 64.0 * nd + 48.0 * td                    # per render = both side launches
     dom_ms = per_tech_ms[dom]
     dom_launch_ms = dom_ms / sides
