@@ -41,20 +41,26 @@ def main():
     tot = sum(v["m"]["gpu__time_duration.sum"] for _, v in last)
     techs = [(l, s) for l in range(1, 8) for s in "NO"]
     print(f"# {title}\n")
-    print("Metrics: `gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum`, `--clock-control none`; the "
+    print("Metrics: `gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum` and the local-memory L1 sectors "
+          "(`l1tex__t_sectors_pipe_lsu_mem_local_op_ld/st.sum`, 32 B each), `--clock-control none`; the "
           f"{len(last)} residual launches of the last step.  Per-launch times are serialised under ncu: compare shares.\n")
-    print("| launch | kernel | technique,side | time ms | share | DRAM read GB | DRAM write GB |")
-    print("|---|---|---|---|---|---|---|")
-    rd = wr = 0.0
+    print("| launch | kernel | technique,side | time ms | share | DRAM read GB | DRAM write GB | local ld GB | local st GB |")
+    print("|---|---|---|---|---|---|---|---|---|")
+    rd = wr = lld = lst = 0.0
     for (k, v), (l, s) in zip(last, techs):
         m = v["m"]
         t = m["gpu__time_duration.sum"]
         rd += m.get("dram__bytes_read.sum", 0)
         wr += m.get("dram__bytes_write.sum", 0)
+        ld = 32 * m.get("l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum", 0)
+        st = 32 * m.get("l1tex__t_sectors_pipe_lsu_mem_local_op_st.sum", 0)
+        lld += ld
+        lst += st
         nm = v["name"].split("(")[0]
         print(f"| {k} | {nm} | T{l},{s} | {t * 1e3:.1f} | {100 * t / tot:.1f}% | {m.get('dram__bytes_read.sum', 0) / 1e9:.1f} | "
-              f"{m.get('dram__bytes_write.sum', 0) / 1e9:.1f} |")
-    print(f"\nStep total: {tot:.2f} s, DRAM read {rd / 1e12:.2f} TB, write {wr / 1e12:.2f} TB ({(rd + wr) / tot / 1e9:.0f} GB/s).")
+              f"{m.get('dram__bytes_write.sum', 0) / 1e9:.1f} | {ld / 1e9:.0f} | {st / 1e9:.0f} |")
+    print(f"\nStep total: {tot:.2f} s, DRAM read {rd / 1e12:.2f} TB, write {wr / 1e12:.2f} TB ({(rd + wr) / tot / 1e9:.0f} GB/s); "
+          f"local-memory traffic through L1: loads {lld / 1e12:.2f} TB, stores {lst / 1e12:.2f} TB.")
 
 
 if __name__ == "__main__":
