@@ -1247,7 +1247,8 @@ typedef struct {
   uint32_t flags;  // 1 TWO_WAY, 2 RECONNECT, 4 REJECT_MULTI, 32 VNDF (GGX visible-normal sampling),
                    // 64 DIAG_ONE_WAY_ABLATION (one-way with the two-way pairing rules; deliberately biased),
                    // 256 NO_PATH_MAPPING (two-way sampling, no mapped paths, static paths rejected),
-                   // 512 T6_TOWARD_LIGHT (T6 directions on the hemisphere toward an emitter)
+                   // 512 T6_TOWARD_LIGHT (T6 directions on the hemisphere toward an emitter),
+                   // 1024 TOBJ_MIDPATH (object transform of the first mid-path hit on a moved object)
   double jacobian_max, alpha_min, dmin_rel;
 } orc_args;
 
@@ -1321,6 +1322,59 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
 
   Gen gp = generate(cx, l, F, st, D);
   Gen gq = nopm ? Gen() : generate(cx, lq, Fb, st, D);  // random-seed replay: same counters
+  // ---- "transform with object movement" on a mid-path hit (RR_TOBJ_MIDPATH; reading 18):
+  // while the pair has not diverged, the first walk vertex x_m (m >= 2) that the base path finds on a MOVED
+  // object is mapped to the same object-space point in the other state, t(x_m) = M_Fbar M_F^-1 x_m (|t'| = 1),
+  // instead of replaying the ray; the mapped walk continues by replay from there.  The edge x_{m-1} -> t(x_m)
+  // must be unoccluded in View_Fbar, else every connection at walk index >= m is rejected; the connections that
+  // use it carry R_T = p_Fbar(t(x_m) | x_{m-1}) / p_F(x_m | x_{m-1}) (walk-order area pdfs).  For the mapping to
+  // stay a bijection, a base vertex x_m on static geometry whose REPLAYED partner lies on a moved object rejects
+  // the pair from m on (that partner maps by t to another path; replaying would map two paths onto x_m's path).
+  const bool single_walk = (l != 3 && l != 6);
+  int mT = -1;
+  bool tobj_fail = false, tobj_reject = false;
+  double RT = 1.0;
+  if ((A.flags & 1024) && paired && single_walk && gp.ok && gq.ok) {
+    const int na = gp.A.n(), nb = gq.A.n();
+    for (int m = 2; m <= na && m - 1 <= nb; ++m) {
+      const int a = m - 1;  // the pair must coincide up to x_{m-1} and leave it in the same direction
+      if (!same_vtx_moved(S.moved, gp.A.v[a], gq.A.v[a])) break;
+      bool pa = a < (int)gp.A.wo_ok.size() && gp.A.wo_ok[a], qa = a < (int)gq.A.wo_ok.size() && gq.A.wo_ok[a];
+      if (!pa || !qa || !same(gp.A.wo[a], gq.A.wo[a])) break;
+      if (S.moved[gp.A.v[m].obj]) {
+        mT = m;
+        break;
+      }
+      if (m <= nb && S.moved[gq.A.v[m].obj]) {  // static base vertex, replayed partner on a moved object
+        mT = m;
+        tobj_reject = true;
+        break;
+      }
+    }
+    if (mT > 0 && !tobj_reject) {
+      const Vtx& x = gp.A.v[mT];
+      const double* MF = &S.xf[F][12 * x.obj];
+      const double* MB = &S.xf[Fb][12 * x.obj];
+      // object space: R_F^T (x - t_F); then placed at M_Fbar (rigid transforms, C7)
+      V3 d = x.p - v3(MF[3], MF[7], MF[11]);
+      V3 po = v3(MF[0] * d.x + MF[4] * d.y + MF[8] * d.z, MF[1] * d.x + MF[5] * d.y + MF[9] * d.z,
+                 MF[2] * d.x + MF[6] * d.y + MF[10] * d.z);
+      V3 no = v3(MF[0] * x.n.x + MF[4] * x.n.y + MF[8] * x.n.z, MF[1] * x.n.x + MF[5] * x.n.y + MF[9] * x.n.z,
+                 MF[2] * x.n.x + MF[6] * x.n.y + MF[10] * x.n.z);
+      Vtx t = x;
+      t.p = xform_point(MB, po);
+      t.n = normalize(v3(MB[0] * no.x + MB[1] * no.y + MB[2] * no.z, MB[4] * no.x + MB[5] * no.y + MB[6] * no.z,
+                         MB[8] * no.x + MB[9] * no.y + MB[10] * no.z));
+      gq.A.v.resize(mT);
+      gq.A.v.push_back(t);
+      if ((int)gq.A.wo.size() > mT) { gq.A.wo.resize(mT); gq.A.wo_ok.resize(mT); }
+      gq.A.pA.resize(mT + 1, 0.0);
+      RT = area_pdf(S, Fb, gq.A.v[mT - 2], gq.A.v[mT - 1], t) / area_pdf(S, F, gp.A.v[mT - 2], gp.A.v[mT - 1], x);
+      tobj_fail = !(RT > 0) || !std::isfinite(RT) ||
+                  !visible(S, Fb, gq.A.v[mT - 1].p, t.p, gq.A.v[mT - 1].tri, t.tri, &cx.C);
+      extend_walk(cx, Fb, st, gq.A, 0, D - 1);  // random-seed replay from t(x_m) on
+    }
+  }
   std::vector<Conn> cp = connections(cx, gp, st, D);
   std::vector<Conn> cq = connections(cx, gq, st, D);
   if (stats) stats->samples++;
@@ -1434,7 +1488,11 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
     if (cq_match) used_q.push_back(cq_match);
     int j = c.walk_index;
     bool recon_here = (w > 0 && single && j >= w + 1 && c.key.kind != 0);
-    if (recon_here) {
+    const bool tobj_here = mT > 0 && j >= mT && c.key.kind != 0;
+    if (tobj_here && (tobj_fail || tobj_reject)) {  // t(x_m) hidden from x_{m-1} in View_Fbar, or the replayed
+      status = ST_REJECTED;                         // partner lies on a moved object: no mapping from x_m on
+      reason = tobj_fail ? RJ_OCCLUDED : RJ_TARGET;
+    } else if (recon_here) {
       if (recon_fail) {
         status = ST_REJECTED;
         reason = recon_reason;
@@ -1476,7 +1534,7 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
             // connection edge: V = 0 zeroes the term, it does not reject
             // R = p_Fbar(suffix | q prefix) / p_F(suffix | p prefix)   (SURVEY 8(c) C7 "R")
             // walk-order vertex m of q: mapped prefix for m <= w, base suffix after
-            R = reconnect_R(S, F, gp.A, gq.A, w, j);
+            R = reconnect_R(S, F, gp.A, gq.A, w, j) * (tobj_here ? RT : 1.0);
             if (!(R > 0) || !std::isfinite(R)) { status = ST_REJECTED; reason = RJ_TARGET; }
             have_q = status == ST_ACCEPTED;
             if (stats && have_q) stats->reconnected++;
@@ -1501,6 +1559,7 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
       const SeedCrossing sq = seed_of(gq, *cq_match);
       eq = eval_path(cx, Fb, q, true, &sq);
       have_q = true;
+      if (tobj_here) R = RT;
     } else {
       status = ST_UNPAIRED;
     }

@@ -40,6 +40,7 @@ VNDF = 32  # GGX directions from the visible normals (Heitz 2018; SURVEY 8(f) ro
 DIAG_ONE_WAY = 64  # RR_DIAG_ONE_WAY_ABLATION: one-way with the two-way pairing rules (biased test mode)
 NO_PATH_MAPPING = 256  # RR_NO_PATH_MAPPING: "incremental w/o PM", with TWO_WAY
 T6_TOWARD_LIGHT = 512  # RR_T6_TOWARD_LIGHT: T6 directions "uniformly toward the light"
+TOBJ_MIDPATH = 1024  # RR_TOBJ_MIDPATH: object transform of a mid-path hit on a moved object
 
 
 @dataclasses.dataclass

@@ -155,6 +155,9 @@ def test_masks_l_plus_7_agree_with_7(cfg, D):
         # T6 "uniformly toward the light": a variance-only change
         t6l = np.stack(p.map(_render, [(cfg_, 12, s, 0x60, S.TWO_WAY | S.T6_TOWARD_LIGHT, D) for s in seeds]))
         _agree(ref, t6l)
+        # T_obj on the first mid-path hit of a moved object: a mapping change only
+        tobj = np.stack(p.map(_render, [(cfg_, 12, s, 0x40, S.TWO_WAY | S.TOBJ_MIDPATH, D) for s in seeds]))
+        _agree(ref, tobj)
 
 
 def test_material_edit_masks_agree():

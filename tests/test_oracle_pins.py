@@ -204,6 +204,8 @@ def test_residual_converges_to_primal_difference(name):
     flags = [S.PAPER_FLAGS, S.TWO_WAY, S.TWO_WAY | S.NO_PATH_MAPPING]
     if name == "c1":  # the T6 variant needs moved objects; on the reveal fixture its splats are heavy-tailed
         flags.append(S.PAPER_FLAGS | S.T6_TOWARD_LIGHT)  # (the paired {6,7} test covers it there)
+    if name != "c2":  # T_obj on mid-path hits of moved objects, with and without reconnection
+        flags += [S.PAPER_FLAGS | S.TOBJ_MIDPATH, S.TWO_WAY | S.TOBJ_MIDPATH]
     ref, res = _runs(name, tuple(flags))
     levels = (1, 4, 16, 64)
     for flags, chunks in res.items():
