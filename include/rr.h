@@ -113,7 +113,15 @@ enum {
                               object e is chosen uniformly (slot-0 d5) and d is uniform on the hemisphere facing e's
                               area-weighted centroid, +d the emitter side; every T6 candidate pdf uses the mixture
                               density (1/n_e) sum_e [d.(c_e - x_G) > 0] / (2 pi).  A variance-only variant (SURVEY
-                              8(f) row 4), compiled as its own kernel instantiation; exclusive with RR_VNDF */
+                              8(f) row 4), compiled into the variants kernel instantiation; exclusive with RR_VNDF */
+  RR_TOBJ_MIDPATH = 1024u,  /* "transform with object movement" on a mid-path hit: while a pair is
+                              undiverged, the first walk vertex x_m (m >= 2) the base path finds on a MOVED object maps
+                              to the same object-space point in the other state, t(x_m) = M_Fbar M_F^-1 x_m
+                              (|t'| = 1), with R_T = ratio of the walk-order area pdfs of x_m and t(x_m); the edge to
+                              t(x_m) must be unoccluded in the other state, and a static base vertex whose replayed
+                              partner lies on a moved object is rejected from there (the mapping stays a bijection).
+                              Single-walk techniques; needs RR_TWO_WAY (or the diagnostic ablation); SURVEY 8(f) row 4,
+                              variants instantiation, exclusive with RR_VNDF */
   RR_DIAG_ONE_WAY_ABLATION = 64u /* DIAGNOSTIC, deliberately biased: one-way
                               (side N only, N_pix*spp samples per technique, RR_TWO_WAY must be off) but with the
                               two-way pairing rules (RR_RECONNECT / RR_REJECT_MULTI allowed); accepted pairs splat

@@ -9,7 +9,7 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "librr_b200.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("rr_capi.cu", "rr_lbvh.cu", "rr_residual.cu", "rr_residual_vndf.cu", "rr_residual_t6l.cu", "rr_primal.cu")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("rr_capi.cu", "rr_lbvh.cu", "rr_residual.cu", "rr_residual_vndf.cu", "rr_residual_var.cu", "rr_primal.cu")]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false", "-prec-div=false", "-prec-sqrt=false", "-std=c++17", "--extended-lambda",
          "-shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 

@@ -735,8 +735,11 @@ static rr_status check_args(rr_ctx* c, const rr_render_args* a) {
     return fail(c, RR_E_INVALID, "RR_NO_PATH_MAPPING needs RR_TWO_WAY without RR_RECONNECT / RR_REJECT_MULTI");
   if ((a->flags & RR_VNDF) && (a->flags & RR_T6_TOWARD_LIGHT))
     return fail(c, RR_E_INVALID, "RR_VNDF and RR_T6_TOWARD_LIGHT are separate kernel variants; choose one");
+  if ((a->flags & RR_TOBJ_MIDPATH) && (!(a->flags & (RR_TWO_WAY | RR_DIAG_ONE_WAY_ABLATION)) || (a->flags & RR_VNDF) ||
+                                      (a->flags & RR_NO_PATH_MAPPING)))
+    return fail(c, RR_E_INVALID, "RR_TOBJ_MIDPATH maps paired paths: needs RR_TWO_WAY (not with RR_VNDF / RR_NO_PATH_MAPPING)");
   if (a->flags & ~(RR_TWO_WAY | RR_RECONNECT | RR_REJECT_MULTI | RR_ACCUMULATE | RR_COUNT_TRAVERSAL | RR_VNDF |
-                   RR_DIAG_ONE_WAY_ABLATION | RR_NO_PATH_MAPPING | RR_T6_TOWARD_LIGHT))
+                   RR_DIAG_ONE_WAY_ABLATION | RR_NO_PATH_MAPPING | RR_T6_TOWARD_LIGHT | RR_TOBJ_MIDPATH))
     return fail(c, RR_E_INVALID, "unknown flag bits");
   if (a->shard_count == 0 || a->shard_index >= a->shard_count) return fail(c, RR_E_INVALID, "bad shard");
   return RR_OK;
@@ -771,6 +774,7 @@ static KArgs make_kargs(rr_ctx* c, const rr_render_args* a, uint32_t mask, int l
   K.mat_type_vndf = (a->flags & RR_VNDF) ? c->mat_type_vndf.p : nullptr;
   K.t6_centroid = (a->flags & RR_T6_TOWARD_LIGHT) ? c->emit_centroid.p : nullptr;
   K.n_centroid = (int)c->emit_centroid.n;
+  K.tobj = (a->flags & RR_TOBJ_MIDPATH) ? 1 : 0;
   K.reconnect = (a->flags & RR_RECONNECT) ? 1 : 0;
   K.reject_multi = (a->flags & RR_REJECT_MULTI) ? 1 : 0;
   K.seed = a->seed;

@@ -34,6 +34,7 @@ struct KArgs {
   const uint32_t* mat_type_vndf;     // RR_VNDF: material types with GGX = 2 (visible-normal sampling), else null
   const float4* t6_centroid;         // RR_T6_TOWARD_LIGHT: emitter centroids (world), else null
   int n_centroid;
+  int tobj;                          // RR_TOBJ_MIDPATH (variants instantiation)
   uint64_t i_begin;
   rr_path_record* recs;
   unsigned long long* rec_count;
@@ -42,7 +43,7 @@ struct KArgs {
 
 void launch_residual(const DevScene& S, const KArgs& A, int grid, cudaStream_t st);
 void launch_residual_vndf(const DevScene& S, const KArgs& A, int grid, cudaStream_t st);  // rr_residual_vndf.cu
-void launch_residual_t6l(const DevScene& S, const KArgs& A, int grid, cudaStream_t st);   // rr_residual_t6l.cu
+void launch_residual_var(const DevScene& S, const KArgs& A, int grid, cudaStream_t st);   // rr_residual_var.cu
 int residual_grid(bool bidir, uint64_t n);  // blocks of residual_block() threads for n sample slots
 int residual_block();
 void launch_primal(const DevScene& S, int F, uint64_t seed, int D, uint32_t spp, float* image,

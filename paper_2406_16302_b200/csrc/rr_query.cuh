@@ -138,7 +138,7 @@ __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay
 // COUNT: count node fetches and triangle tests (rr_stats.nodes_visited / tris_tested; off in timed renders,
 // where the two counters cost ~3%).  Inlined into its call site: under the 32-register budget a call boundary
 // forces the scene pointers through generic loads and spills (-9% on config 4 when inlined).
-#if defined(RR_T6L_KERNELS) && RR_T6L_KERNELS
+#if defined(RR_VAR_KERNELS) && RR_VAR_KERNELS
 // RR_T6_TOWARD_LIGHT: 4 pi p_dir(d | x) of T6's direction d at a ghost point x (the oracle's t6_pdir):
 // (2 / n_e) #{e : d . (c_e - x) > 0}; 1 for the uniform sphere
 __device__ __forceinline__ float t6_pdir4pi(const float4* c, int n, float3 x, float3 d) {
@@ -153,7 +153,7 @@ __device__ __forceinline__ float t6_pdir4pi(const float4* c, int n, float3 x, fl
 
 template <bool COUNT>
 __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRes& r, QCount& qc
-#if defined(RR_T6L_KERNELS) && RR_T6L_KERNELS
+#if defined(RR_VAR_KERNELS) && RR_VAR_KERNELS
                                           , const float4* t6c, int t6n
 #endif
 ) {
@@ -225,10 +225,10 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
         float4 a4 = __ldg(tp), b4 = __ldg(tp + 1), c4 = __ldg(tp + 2);
         float3 nrm = norm3_exact(cross3(f3(b4.x - a4.x, b4.y - a4.y, b4.z - a4.z), f3(c4.x - a4.x, c4.y - a4.y, c4.z - a4.z)));
         float inv_c = 1.0f / fabsf(dot3(nrm, d));
-#if defined(RR_T6L_KERNELS) && RR_T6L_KERNELS
+#if defined(RR_VAR_KERNELS) && RR_VAR_KERNELS
         // s0 carries 4 pi p_dir of the path's direction through this crossing (T6's candidate pdf)
         const float3 xw = q.o + q.d * t;
-        const float pd = t6_pdir4pi(t6c, t6n, xw, q.rev ? q.d * -1.0f : q.d);
+        const float pd = t6c ? t6_pdir4pi(t6c, t6n, xw, q.rev ? q.d * -1.0f : q.d) : 1.0f;
 #else
         const float pd = 1.0f;
 #endif
@@ -279,7 +279,7 @@ __device__ __forceinline__ Query mk_ray(P3 o, float3 d, int excl, int want) {
   q.type = QT_CLOSEST;
   q.want = (uint8_t)want;
   q.dyn_only = 0;
-#if defined(RR_T6L_KERNELS) && RR_T6L_KERNELS
+#if defined(RR_VAR_KERNELS) && RR_VAR_KERNELS
   q.rev = 0;
 #endif
   q.seed_t = 0.0f;
@@ -297,7 +297,7 @@ __device__ __forceinline__ Query mk_seg(P3 a, P3 b, int ea, int eb, int want, bo
   q.type = QT_SEG;
   q.want = (uint8_t)want;
   q.dyn_only = dyn_only ? 1 : 0;
-#if defined(RR_T6L_KERNELS) && RR_T6L_KERNELS
+#if defined(RR_VAR_KERNELS) && RR_VAR_KERNELS
   q.rev = 0;
 #endif
   q.seed_t = 0.0f;

@@ -17,8 +17,8 @@
 #ifndef RR_VNDF_KERNELS
 #define RR_VNDF_KERNELS 0  // 1: this TU is the RR_VNDF instantiation (rr_residual_vndf.cu)
 #endif
-#ifndef RR_T6L_KERNELS
-#define RR_T6L_KERNELS 0  // 1: this TU is the RR_T6_TOWARD_LIGHT instantiation (rr_residual_t6l.cu)
+#ifndef RR_VAR_KERNELS
+#define RR_VAR_KERNELS 0  // 1: this TU is the mapping-variants instantiation (rr_residual_var.cu)
 #endif
 #include <cuda_runtime.h>
 
@@ -35,13 +35,13 @@ namespace rr {
 // visible-normal sampling compiled in), so that the default kernels carry no code of the variant
 #if RR_VNDF_KERNELS
 namespace kvndf {
-#elif RR_T6L_KERNELS
-namespace kt6l {
+#elif RR_VAR_KERNELS
+namespace kvar {
 #else
 namespace kplain {
 #endif
-// RR_T6_TOWARD_LIGHT (kt6l only): the path runs this query's edge against its direction (crossing p_dir)
-#if RR_T6L_KERNELS
+// RR_T6_TOWARD_LIGHT (kvar only): the path runs this query's edge against its direction (crossing p_dir)
+#if RR_VAR_KERNELS
 __device__ __forceinline__ Query orient(Query q, bool rev) {
   q.rev = rev ? 1 : 0;
   return q;
@@ -116,6 +116,12 @@ struct SState {
   PV L;
   int pixp, pixq;
   float3 woP, woQ;
+#if RR_VAR_KERNELS
+  // RR_TOBJ_MIDPATH: walk index of the mapped vertex t(x_m) (0 none), its state (1 visibility pending, 2 mapped,
+  // 3 occluded, 4 static base vertex with a replayed partner on a moved object) and R_T
+  int tobj_m, tobj_st, q_tobj;
+  float RT;
+#endif
 };
 
 __device__ __forceinline__ bool nee_ok(int tech, int m) { return tech == 2 ? m >= 2 : true; }
@@ -217,6 +223,11 @@ __device__ __forceinline__ void single_issue(const DevScene& S, const KArgs& A, 
   if (hasQ && edited(S, Q.v[m].obj)) st.dynQ++;
   if (st.recon == 3)
     st.q_recon = B.push(RR_ORIENT(mk_seg(Q.v[st.w].p, P.v[st.w + 1].p, Q.v[st.w].tri, P.v[st.w + 1].tri, bit(Fb)), Lroot));
+#if RR_VAR_KERNELS
+  st.q_tobj = -1;
+  if (st.tobj_st == 1)  // x_{m-1} -> t(x_m) in View_Fbar, and the edge's ghost crossings for Q's MIS
+    st.q_tobj = B.push(RR_ORIENT(mk_seg(Q.v[m - 1].p, Q.v[m].p, Q.v[m - 1].tri, Q.v[m].tri, bit(Fb)), Lroot));
+#endif
   if (st.suffix_pending)
     st.q_suffix = B.push(RR_ORIENT(mk_seg(P.v[m - 1].p, P.v[m].p, P.v[m - 1].tri, P.v[m].tri, bit(Fb), true), Lroot));
   float d[8];
@@ -294,6 +305,14 @@ __device__ __forceinline__ bool single_consume(const DevScene& S, const KArgs& A
   PV E = cam_pv(S);
   const uint64_t i = st.i;
   bool hasP = m <= P.n, hasQ = m <= Q.n;
+#if RR_VAR_KERNELS
+  if (st.q_tobj >= 0) {
+    const QRes& r = B.r[st.q_tobj];
+    st.tobj_st = r.ok[Fb] ? 2 : 3;
+    Q.ex[m] = r.c[Fb];
+    if (st.tobj_st == 3) st.Qend = true;  // no mapped path from x_m on
+  }
+#endif
   // ---- pending reconnection edge (checked in View_Fbar)
   if (st.q_recon >= 0) {
     const QRes& r = B.r[st.q_recon];
@@ -353,6 +372,11 @@ __device__ __forceinline__ bool single_consume(const DevScene& S, const KArgs& A
     if (st.pc_) {
       int stt = ST_ACCEPTED, rs = RJ_NONE;
       float R = 1.0f;
+#if RR_VAR_KERNELS
+      const bool tobj_here = st.tobj_m > 0 && m >= st.tobj_m;
+      if (tobj_here && st.tobj_st >= 3) { stt = ST_REJECTED; rs = st.tobj_st == 3 ? RJ_OCCLUDED : RJ_TARGET; }
+      else
+#endif
       if (st.recon == 2 && m >= st.w + 1) { stt = ST_REJECTED; rs = st.reject_reason; }
       else if (reconnected_here && m >= st.reject_from) { stt = ST_REJECTED; rs = st.reject_reason; }
       else if (!qc_) stt = ST_UNPAIRED;
@@ -360,6 +384,9 @@ __device__ __forceinline__ bool single_consume(const DevScene& S, const KArgs& A
         R = st.R1 * (m >= st.w + 2 ? st.R2 : 1.0f);
         if (!(R > 0.0f) || !isfinite(R)) { stt = ST_REJECTED; rs = RJ_TARGET; }
       }
+#if RR_VAR_KERNELS
+      if (tobj_here && stt == ST_ACCEPTED) R *= st.RT;  // the object-transformed vertex (R_T; reading 18)
+#endif
       if (stt == ST_ACCEPTED && A.reject_multi && st.hdiv && (st.dynP >= 2 || st.dynQ >= 2)) { stt = ST_REJECTED; rs = RJ_MULTI; }
       finish(o, i, kind, m, 0, stt, rs, pixp, vp, pixq, vq, R);
     } else if (qc_ && !A.two_way) {
@@ -385,6 +412,33 @@ __device__ __forceinline__ bool single_consume(const DevScene& S, const KArgs& A
       } else {
         st.Qend = true;
       }
+#if RR_VAR_KERNELS
+      // RR_TOBJ_MIDPATH: on the undiverged pair's first mid-path hit of a MOVED object the mapped
+      // vertex is the same object-space point in Fbar, t(x) = M_Fbar M_F^-1 x (|t'| = 1), instead of the replayed
+      // hit; a static base vertex whose replayed partner lies on a moved object rejects the pair from there on
+      if (A.tobj && st.tobj_st == 0) {
+        const bool pm = gotP && (oflags(S, P.v[m + 1].obj) & OBJ_MOVED);
+        const bool qm = r.ok[Fb] && (oflags(S, Q.v[m + 1].obj) & OBJ_MOVED);
+        if (pm) {
+          const PV& x = P.v[m + 1];
+          const DevInstance& I = S.inst[__ldg(&S.obj_inst[x.obj])];
+          PV t = x;
+          t.p = xf_point_d(I.M[Fb], xf_point_d(I.Mi[F], x.p));
+          t.n = norm3_exact(xf_vec(I.M[Fb], xf_vec(I.Mi[F], x.n)));
+          Q.v[m + 1] = t;
+          Q.n = m + 1;
+          st.Qend = false;
+          st.tobj_m = m + 1;
+          st.tobj_st = 1;  // visibility of Q.v[m] -> t with the next batch
+          st.RT = area_pdf(S, Fb, Q.v[m - 1], Q.v[m], t) / area_pdf(S, F, P.v[m - 1], P.v[m], x);
+          if (!(st.RT > 0.0f) || !isfinite(st.RT)) { st.tobj_st = 3; st.Qend = true; }
+        } else if (qm) {
+          st.tobj_m = m + 1;
+          st.tobj_st = 4;
+          st.Qend = true;
+        }
+      }
+#endif
     }
   }
   if (hasP && !gotP) st.Pend = true;
@@ -494,6 +548,10 @@ __device__ __forceinline__ bool single_step(const DevScene& S, const KArgs& A, S
       st.reject_reason = RJ_NONE;
       st.R1 = st.R2 = 1.0f;
       st.rdiv = st.hdiv = st.suffix_pending = false;
+#if RR_VAR_KERNELS
+      st.tobj_m = st.tobj_st = 0;
+      st.RT = 1.0f;
+#endif
       st.dynP = st.dynQ = 0;
       st.Pend = st.P.n == 0;
       st.Qend = st.Q.n == 0;
@@ -568,15 +626,23 @@ __device__ void bidir_start_issue(const DevScene& S, const KArgs& A, int tech, i
   } else {
     if (S.n_moved == 0 || D < 3) return;
     PV xg = sample_set(S, S.moved_tris, S.moved_cdf, S.n_moved, 1 - F, d0[0], d0[1], d0[2]);
-#if RR_T6L_KERNELS
-    // "uniformly toward the light": emitter e from d5, d uniform on the hemisphere about c_e - x_G
-    const int e = min((int)floorf(d0[5] * (float)A.n_centroid), A.n_centroid - 1);
-    const float4 ce = __ldg(A.t6_centroid + e);
-    const float3 ax = norm3_exact(sub3(make_double3(ce.x, ce.y, ce.z), xg.p));
-    float z = d0[3];
-    float rr = sqrtf(fmaxf(0.0f, 1.0f - z * z)), s, c;
-    sincosf(2.0f * RR_PI_F * d0[4], &s, &c);
-    float3 dir = norm3_exact(to_world(ax, rr * c, rr * s, z));
+#if RR_VAR_KERNELS
+    float3 dir;
+    if (A.t6_centroid) {
+      // "uniformly toward the light": emitter e from d5, d uniform on the hemisphere about c_e - x_G
+      const int e = min((int)floorf(d0[5] * (float)A.n_centroid), A.n_centroid - 1);
+      const float4 ce = __ldg(A.t6_centroid + e);
+      const float3 ax = norm3_exact(sub3(make_double3(ce.x, ce.y, ce.z), xg.p));
+      float z = d0[3];
+      float rr = sqrtf(fmaxf(0.0f, 1.0f - z * z)), s, c;
+      sincosf(2.0f * RR_PI_F * d0[4], &s, &c);
+      dir = norm3_exact(to_world(ax, rr * c, rr * s, z));
+    } else {  // uniform sphere
+      float z = 1.0f - 2.0f * d0[3];
+      float rr = 2.0f * sqrtf(d0[3] * (1.0f - d0[3])), s, c;
+      sincosf(2.0f * RR_PI_F * d0[4], &s, &c);
+      dir = f3(rr * c, rr * s, z);
+    }
 #else
     float z = 1.0f - 2.0f * d0[3];
     float rr = 2.0f * sqrtf(d0[3] * (1.0f - d0[3])), s, c;  // sqrt(1 - z^2), no cancellation
@@ -657,8 +723,8 @@ __device__ void bidir_consume(const DevScene& S, const KArgs& A, int F, BPath& G
   if (G.qyz >= 0) {  // crossings of the edge y_1 -> z_1, plus the crossing at x_G
     const float3 dv = sub3(G.A.v[1].p, G.A.v[0].p);
     const float L = norm3f(dv);
-#if RR_T6L_KERNELS
-    const float pd = t6_pdir4pi(A.t6_centroid, A.n_centroid, f3of(G.start.p), G.dir0);  // +d: z_1 -> y_1
+#if RR_VAR_KERNELS
+    const float pd = A.t6_centroid ? t6_pdir4pi(A.t6_centroid, A.n_centroid, f3of(G.start.p), G.dir0) : 1.0f;  // +d: z_1 -> y_1
 #else
     const float pd = 1.0f;
 #endif
@@ -907,7 +973,7 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
     }
     sc[4] += active;
     for (int k = 0; k < nmax; ++k)
-#if RR_T6L_KERNELS
+#if RR_VAR_KERNELS
       if (k < B.n) run_query<COUNT>(S, B.q[k], B.r[k], o.qc, A.t6_centroid, A.n_centroid);
 #else
       if (k < B.n) run_query<COUNT>(S, B.q[k], B.r[k], o.qc);
@@ -966,9 +1032,9 @@ inline void launch_kernels(const DevScene& S, const KArgs& A, int grid, cudaStre
 }
 }  // namespace kplain / kvndf
 
-#if RR_T6L_KERNELS
-void launch_residual_t6l(const DevScene& S, const KArgs& A, int grid, cudaStream_t st) {
-  kt6l::launch_kernels(S, A, grid, st);
+#if RR_VAR_KERNELS
+void launch_residual_var(const DevScene& S, const KArgs& A, int grid, cudaStream_t st) {
+  kvar::launch_kernels(S, A, grid, st);
 }
 #elif RR_VNDF_KERNELS
 void launch_residual_vndf(const DevScene& S0, const KArgs& A, int grid, cudaStream_t st) {
@@ -1059,7 +1125,7 @@ int residual_grid(bool bidir, uint64_t n) {
 }
 int residual_block() { return RR_BLOCK; }
 void launch_residual(const DevScene& S, const KArgs& A, int grid, cudaStream_t st) {
-  if (A.t6_centroid) launch_residual_t6l(S, A, grid, st);  // RR_T6_TOWARD_LIGHT: its own instantiation
+  if (A.t6_centroid || A.tobj) launch_residual_var(S, A, grid, st);  // SURVEY 8(f) row 4 variants: their own kernels
   else if (A.mat_type_vndf) launch_residual_vndf(S, A, grid, st);  // RR_VNDF: the other instantiation
   else kplain::launch_kernels(S, A, grid, st);
 }
@@ -1073,5 +1139,5 @@ void launch_segment(const DevScene& S, uint32_t n, const float* segs, float* out
   k_segment<<<(n + 127) / 128, 128, 0, st>>>(S, n, segs, out);
 }
 
-#endif  // RR_VNDF_KERNELS / RR_T6L_KERNELS
+#endif  // RR_VNDF_KERNELS / RR_VAR_KERNELS
 }  // namespace rr

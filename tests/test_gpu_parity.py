@@ -317,10 +317,25 @@ def test_records_diag_one_way_config1(torch_cuda):
 @pytest.mark.parametrize("cfg", ["c1", "rev", 3, 4, 5])
 def test_records_t6_toward_light(torch_cuda, cfg):
     """RR_T6_TOWARD_LIGHT: T6 directions on the hemisphere toward an emitter, and every
-    path's T6 candidate pdf with the mixture direction density (its own kernel instantiation, rr_residual_t6l.cu)."""
+    path's T6 candidate pdf with the mixture direction density (its own kernel instantiation, rr_residual_var.cu)."""
     w = {"c1": S.config1, "rev": lambda: S.occluder_reveal(32, 32, spp=8, max_depth=5)}.get(cfg, lambda: S.load_config(cfg))()
     args = dataclasses.replace(w.args, flags=S.PAPER_FLAGS | S.T6_TOWARD_LIGHT)
     if cfg in ("c1", "rev"):
+        record_parity(w, args)
+    else:
+        record_parity(w, args, n_per=1024, strided=True)
+
+
+@pytest.mark.parametrize("cfg,flags", [("c1", S.PAPER_FLAGS), ("c1", S.TWO_WAY), ("rev", S.PAPER_FLAGS),
+                                       ("c1d6", S.PAPER_FLAGS | S.T6_TOWARD_LIGHT), (3, S.PAPER_FLAGS),
+                                       (4, S.PAPER_FLAGS), (5, S.PAPER_FLAGS)])
+def test_records_tobj_midpath(torch_cuda, cfg, flags):
+    """RR_TOBJ_MIDPATH ("transform with object movement"): the first mid-path hit
+    of a moved object maps by the object transform (variants instantiation, rr_residual_var.cu)."""
+    w = {"c1": S.config1, "c1d6": lambda: S.config1(32, 32, spp=4, max_depth=6),
+         "rev": lambda: S.occluder_reveal(32, 32, spp=8, max_depth=5)}.get(cfg, lambda: S.load_config(cfg))()
+    args = dataclasses.replace(w.args, flags=flags | S.TOBJ_MIDPATH)
+    if isinstance(cfg, str):
         record_parity(w, args)
     else:
         record_parity(w, args, n_per=1024, strided=True)
@@ -487,7 +502,8 @@ def test_invalid_arguments_are_refused(torch_cuda):
     for bad in (dict(technique_mask=0x3F), dict(spp=3), dict(max_depth=0), dict(max_depth=11),
                 dict(flags=S.RECONNECT), dict(layer_mask=0x80), dict(flags=S.PAPER_FLAGS | 1024),
                 dict(flags=S.PAPER_FLAGS | S.DIAG_ONE_WAY), dict(flags=S.PAPER_FLAGS | S.NO_PATH_MAPPING),
-                dict(flags=S.NO_PATH_MAPPING), dict(flags=S.PAPER_FLAGS | S.VNDF | S.T6_TOWARD_LIGHT)):
+                dict(flags=S.NO_PATH_MAPPING), dict(flags=S.PAPER_FLAGS | S.VNDF | S.T6_TOWARD_LIGHT),
+                dict(flags=S.TOBJ_MIDPATH), dict(flags=S.PAPER_FLAGS | S.VNDF | S.TOBJ_MIDPATH)):
         with pytest.raises(RRError):
             r.render_residual(dataclasses.replace(w.args, **bad))
     for bad in (dict(state=2), dict(spp=0), dict(max_depth=0), dict(max_depth=11)):
