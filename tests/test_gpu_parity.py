@@ -500,7 +500,7 @@ def test_invalid_arguments_are_refused(torch_cuda):
     w = S.config1(16, 16)
     r = _renderer(w)
     for bad in (dict(technique_mask=0x3F), dict(spp=3), dict(max_depth=0), dict(max_depth=11),
-                dict(flags=S.RECONNECT), dict(layer_mask=0x80), dict(flags=S.PAPER_FLAGS | 1024),
+                dict(flags=S.RECONNECT), dict(layer_mask=0x80), dict(flags=S.PAPER_FLAGS | 2048),
                 dict(flags=S.PAPER_FLAGS | S.DIAG_ONE_WAY), dict(flags=S.PAPER_FLAGS | S.NO_PATH_MAPPING),
                 dict(flags=S.NO_PATH_MAPPING), dict(flags=S.PAPER_FLAGS | S.VNDF | S.T6_TOWARD_LIGHT),
                 dict(flags=S.TOBJ_MIDPATH), dict(flags=S.PAPER_FLAGS | S.VNDF | S.TOBJ_MIDPATH)):

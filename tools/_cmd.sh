@@ -1,2 +1,2 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-for v in b12 b10 b8; do echo "== $v"; RR_LIB_VARIANT=build/variants/$v.so python tools/timing.py 3,4 2>&1 | grep "config\|per launch"; done
+timeout 1500 python -m pytest tests -m gpu -q -k "tobj or t6_toward or invalid" > gpurun_out/pt.log 2>&1; echo "pytest $?"; tail -5 gpurun_out/pt.log; grep -E "^E .*Assert" gpurun_out/pt.log | cut -c1-700 | head -6
