@@ -20,6 +20,13 @@
 namespace rr {
 
 enum { QT_CLOSEST = 0, QT_SEG = 1 };
+// cache policy of the BVH node / leaf-row loads (tuning knob; __ldg = read-only path through L1)
+#ifndef RR_NODE_LD
+#define RR_NODE_LD __ldg
+#endif
+#ifndef RR_TRI_LD
+#define RR_TRI_LD __ldg
+#endif
 
 
 
@@ -72,7 +79,7 @@ __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay
     if (node >= 0) {
       if (COUNT) nn++;
       const float4* nd = S.nodes + 4 * node;
-      float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
+      float4 n0 = RR_NODE_LD(nd), n1 = RR_NODE_LD(nd + 1), n2 = RR_NODE_LD(nd + 2), n3 = RR_NODE_LD(nd + 3);
       bool h0, h1;
       float t0, t1;
       box2(r, n0, n1, n2, tmin, tmax, h0, h1, t0, t1);
@@ -103,17 +110,17 @@ __device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay
       if (COUNT) nt++;
       // unit-triangle test (Woop 2004): plane distance, then barycentrics u, v of the plane point
       const float4* xp = S.lxf + 3 * li;
-      const float4 m2 = __ldg(xp + 2);
+      const float4 m2 = RR_TRI_LD(xp + 2);
       // explicit FMAs (the library builds with -fmad=false; rounding here is the same for both states)
       const float oz = fmaf(m2.x, r.o.x, fmaf(m2.y, r.o.y, fmaf(m2.z, r.o.z, m2.w)));
       const float dz = fmaf(m2.x, r.d.x, fmaf(m2.y, r.d.y, m2.z * r.d.z));
       const float t = __fdividef(-oz, dz);  // 2 ulp; the hit point itself is recomputed in fp64 (hit_pv)
       if (t > tmin && t < tmax) {
-        const float4 m0 = __ldg(xp);
+        const float4 m0 = RR_TRI_LD(xp);
         const float u = fmaf(t, fmaf(m0.x, r.d.x, fmaf(m0.y, r.d.y, m0.z * r.d.z)),
                              fmaf(m0.x, r.o.x, fmaf(m0.y, r.o.y, fmaf(m0.z, r.o.z, m0.w))));
         if (u >= 0.0f && u <= 1.0f) {
-          const float4 m1 = __ldg(xp + 1);
+          const float4 m1 = RR_TRI_LD(xp + 1);
           const float v = fmaf(t, fmaf(m1.x, r.d.x, fmaf(m1.y, r.d.y, m1.z * r.d.z)),
                                fmaf(m1.x, r.o.x, fmaf(m1.y, r.o.y, fmaf(m1.z, r.o.z, m1.w))));
           if (v >= 0.0f && u + v <= 1.0f) {
