@@ -1248,7 +1248,8 @@ typedef struct {
                    // 64 DIAG_ONE_WAY_ABLATION (one-way with the two-way pairing rules; deliberately biased),
                    // 256 NO_PATH_MAPPING (two-way sampling, no mapped paths, static paths rejected),
                    // 512 T6_TOWARD_LIGHT (T6 directions on the hemisphere toward an emitter),
-                   // 1024 TOBJ_MIDPATH (object transform of the first mid-path hit on a moved object)
+                   // 1024 TOBJ_MIDPATH (object transform of the first mid-path hit on a moved object),
+                   // 2048 RECONNECT_BIDIR (reconnection inside the T3 / T6 emitter-side sub-walk)
   double jacobian_max, alpha_min, dmin_rel;
 } orc_args;
 
@@ -1421,6 +1422,49 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
     }
   }
 
+  // ---- reconnection inside the two-ended techniques' emitter-side sub-walk (RR_RECONNECT_BIDIR, P:L387-411;
+  // DESIGN.md reading 19): the single-walk rule applied to walk B (v[0] = x_D for T3, z_1 for T6; v[1..] = y):
+  // the first index where the pair is diverged and both vertices are rough reconnects the mapped y'_w to the
+  // base's y_{w+1}, with the same target conditions, rejections and R; at most one reconnection per path (the
+  // sensor-side walk stays replayed).
+  int wB = -1;
+  bool reconB_fail = false;
+  int reconB_reason = RJ_NONE;
+  if (reconnect && !single && (A.flags & 2048) && gp.ok && gq.ok) {
+    bool div = false;
+    const int na = gp.B.n(), nb = gq.B.n();
+    for (int m = 1; m <= std::min(na, nb); ++m) {
+      const Vtx& a = gp.B.v[m];
+      const Vtx& b = gq.B.v[m];
+      if (!same_vtx_moved(S.moved, a, b) || !same_vtx_moved(S.moved, gp.B.v[m - 1], gq.B.v[m - 1])) div = true;
+      bool a_ok = m < (int)gp.B.wo_ok.size() && gp.B.wo_ok[m];
+      bool b_ok = m < (int)gq.B.wo_ok.size() && gq.B.wo_ok[m];
+      bool dir_div = (a_ok != b_ok) || (a_ok && b_ok && !same(gp.B.wo[m], gq.B.wo[m]));
+      if ((div || dir_div) && roughness(mat_of(S, a.obj, F)) >= A.alpha_min &&
+          roughness(mat_of(S, b.obj, Fb)) >= A.alpha_min) {
+        wB = m;
+        break;
+      }
+      if (dir_div) div = true;
+    }
+    if (wB > 0 && wB + 1 <= na) {
+      const Vtx& vw = gp.B.v[wB];
+      const Vtx& vq = gq.B.v[wB];
+      const Vtx& t1 = gp.B.v[wB + 1];
+      double dmin = A.dmin_rel * S.diag;
+      if (S.edited[t1.obj]) { reconB_fail = true; reconB_reason = RJ_TARGET; }
+      else if (roughness(mat_of(S, t1.obj, F)) < A.alpha_min) { reconB_fail = true; reconB_reason = RJ_TARGET; }
+      else if (std::min(len(vw.p - t1.p), len(vq.p - t1.p)) < dmin) { reconB_fail = true; reconB_reason = RJ_TARGET; }
+      else if (!visible(S, Fb, vq.p, t1.p, vq.tri, t1.tri, &cx.C)) { reconB_fail = true; reconB_reason = RJ_OCCLUDED; }
+      else {
+        V3 a = normalize(vq.p - t1.p), b = normalize(vw.p - t1.p);
+        double Jg = std::fabs(dot(t1.n, a)) / std::fabs(dot(t1.n, b)) * dot(vw.p - t1.p, vw.p - t1.p) /
+                    dot(vq.p - t1.p, vq.p - t1.p);
+        if (!(Jg <= A.jacobian_max && Jg >= 1.0 / A.jacobian_max)) { reconB_fail = true; reconB_reason = RJ_JACOBIAN; }
+      }
+    }
+  }
+
   auto find_q = [&](const Key& k) -> const Conn* {
     for (const Conn& c : cq)
       if (c.key == k) return &c;
@@ -1551,6 +1595,43 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
                 o.push_back(v->n.x); o.push_back(v->n.y); o.push_back(v->n.z);
               }
             }
+          }
+        }
+      }
+    } else if (wB > 0 && c.key.kind == 3 && c.key.b >= wB + 1) {  // reconnected emitter side (reading 19)
+      const int t = c.key.a, sb = c.key.b;
+      if (reconB_fail) {
+        status = ST_REJECTED;
+        reason = reconB_reason;
+      } else if (t > gq.A.n()) {
+        status = ST_UNPAIRED;  // the mapped sensor side lacks z'_t
+      } else {
+        for (int m = wB + 2; m <= sb; ++m)
+          if (S.edited[gp.B.v[m].obj]) { status = ST_REJECTED; reason = RJ_SUFFIX_DYN; }
+        if (status == ST_ACCEPTED) {
+          q.x.push_back(c.path.x.front());
+          for (int m = t; m >= 1; --m) q.x.push_back(gq.A.v[m]);
+          if (l == 3) q.x.push_back(gq.start);
+          for (int m = 1; m <= wB; ++m) q.x.push_back(gq.B.v[m]);
+          for (int m = wB + 1; m <= sb; ++m) q.x.push_back(gp.B.v[m]);
+          q.x.push_back(c.path.x.back());  // the same NEE vertex (slot 16 + s)
+          q.pixel = project(S, gq.A.v[t].p);
+          SeedCrossing sq;
+          if (gq.tech == 6) {
+            sq.edge = t;
+            sq.p = gq.start.p;
+            sq.n = gq.start.n;
+            sq.tri = gq.start.tri;
+          }
+          eq = eval_path(cx, Fb, q, true, &sq);
+          const int k = (int)q.x.size();
+          for (int e = 1; e < k - 2; ++e)  // every walk edge of q (the two connection edges only zero V)
+            if (!eq.edge_vis[e]) { status = ST_REJECTED; reason = RJ_OCCLUDED; }
+          if (status == ST_ACCEPTED) {
+            R = reconnect_R(S, F, gp.B, gq.B, wB, sb);
+            if (!(R > 0) || !std::isfinite(R)) { status = ST_REJECTED; reason = RJ_TARGET; }
+            have_q = status == ST_ACCEPTED;
+            if (stats && have_q) stats->reconnected++;
           }
         }
       }

@@ -158,6 +158,11 @@ def test_masks_l_plus_7_agree_with_7(cfg, D):
         # T_obj on the first mid-path hit of a moved object: a mapping change only
         tobj = np.stack(p.map(_render, [(cfg_, 12, s, 0x40, S.TWO_WAY | S.TOBJ_MIDPATH, D) for s in seeds]))
         _agree(ref, tobj)
+        # reconnection inside the two-ended techniques' emitter-side sub-walk
+        for l in (3, 6):
+            rb = np.stack(p.map(_render, [(cfg_, 12, s, 0x40 | (1 << (l - 1)), S.PAPER_FLAGS | S.RECONNECT_BIDIR, D)
+                                          for s in seeds]))
+            _agree(ref, rb)
 
 
 def test_material_edit_masks_agree():
@@ -165,6 +170,7 @@ def test_material_edit_masks_agree():
     with _pool() as p:
         ref = np.stack(p.map(_render, [(2, 12, s, 0x40, S.TWO_WAY, 4) for s in seeds]))
         for mask, flags in ((0x47, S.TWO_WAY), (0x47, S.PAPER_FLAGS), (0x41, S.PAPER_FLAGS), (0x44, S.TWO_WAY),
+                            (0x44, S.PAPER_FLAGS | S.RECONNECT_BIDIR),
                             (0x47, S.PAPER_FLAGS | S.VNDF), (0x44, S.TWO_WAY | S.VNDF), (0x40, S.VNDF)):
             other = np.stack(p.map(_render, [(2, 12, s, mask, flags, 4) for s in seeds]))
             _agree(ref, other, pix_frac=0.95)  # GGX alpha 0.1 light-tracing splats are heavy-tailed

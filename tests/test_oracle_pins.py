@@ -206,6 +206,7 @@ def test_residual_converges_to_primal_difference(name):
         flags.append(S.PAPER_FLAGS | S.T6_TOWARD_LIGHT)  # (the paired {6,7} test covers it there)
     if name != "c2":  # T_obj on mid-path hits of moved objects, with and without reconnection
         flags += [S.PAPER_FLAGS | S.TOBJ_MIDPATH, S.TWO_WAY | S.TOBJ_MIDPATH]
+    flags.append(S.PAPER_FLAGS | S.RECONNECT_BIDIR)  # reconnection inside the T3 / T6 sub-walks
     ref, res = _runs(name, tuple(flags))
     levels = (1, 4, 16, 64)
     for flags, chunks in res.items():

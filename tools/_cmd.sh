@@ -1,3 +1,3 @@
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-python tools/timing.py 4 2>&1 | grep "config\|per launch"
-for v in ncg tcg ntcg nlu; do echo "== $v"; RR_LIB_VARIANT=build/variants/$v.so python tools/timing.py 4 2>&1 | grep "config\|per launch"; done
+bash tools/gpu_tests.sh
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 2>&1 | tail -1
