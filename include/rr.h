@@ -122,6 +122,12 @@ enum {
                               partner lies on a moved object is rejected from there (the mapping stays a bijection).
                               Single-walk techniques; needs RR_TWO_WAY (or the diagnostic ablation); SURVEY 8(f) row 4,
                               variants instantiation, exclusive with RR_VNDF */
+  RR_RECONNECT_BIDIR = 2048u, /* reconnection inside the two-ended techniques (T3 / T6): the single-
+                              walk rule applied to the emitter-side sub-walk -- at its first index where the pair is
+                              diverged and both vertices are rough the mapped y'_w reconnects to the base's y_{w+1}
+                              (same target conditions, Jacobian band, rejections and R); the sensor side stays
+                              replayed, so a path reconnects at most once.  Needs RR_RECONNECT; SURVEY 8(f) row 4,
+                              variants instantiation, exclusive with RR_VNDF */
   RR_DIAG_ONE_WAY_ABLATION = 64u /* DIAGNOSTIC, deliberately biased: one-way
                               (side N only, N_pix*spp samples per technique, RR_TWO_WAY must be off) but with the
                               two-way pairing rules (RR_RECONNECT / RR_REJECT_MULTI allowed); accepted pairs splat

@@ -738,8 +738,11 @@ static rr_status check_args(rr_ctx* c, const rr_render_args* a) {
   if ((a->flags & RR_TOBJ_MIDPATH) && (!(a->flags & (RR_TWO_WAY | RR_DIAG_ONE_WAY_ABLATION)) || (a->flags & RR_VNDF) ||
                                       (a->flags & RR_NO_PATH_MAPPING)))
     return fail(c, RR_E_INVALID, "RR_TOBJ_MIDPATH maps paired paths: needs RR_TWO_WAY (not with RR_VNDF / RR_NO_PATH_MAPPING)");
+  if ((a->flags & RR_RECONNECT_BIDIR) && (!(a->flags & RR_RECONNECT) || (a->flags & RR_VNDF)))
+    return fail(c, RR_E_INVALID, "RR_RECONNECT_BIDIR extends RR_RECONNECT (not with RR_VNDF)");
   if (a->flags & ~(RR_TWO_WAY | RR_RECONNECT | RR_REJECT_MULTI | RR_ACCUMULATE | RR_COUNT_TRAVERSAL | RR_VNDF |
-                   RR_DIAG_ONE_WAY_ABLATION | RR_NO_PATH_MAPPING | RR_T6_TOWARD_LIGHT | RR_TOBJ_MIDPATH))
+                   RR_DIAG_ONE_WAY_ABLATION | RR_NO_PATH_MAPPING | RR_T6_TOWARD_LIGHT | RR_TOBJ_MIDPATH |
+                   RR_RECONNECT_BIDIR))
     return fail(c, RR_E_INVALID, "unknown flag bits");
   if (a->shard_count == 0 || a->shard_index >= a->shard_count) return fail(c, RR_E_INVALID, "bad shard");
   return RR_OK;
@@ -775,6 +778,7 @@ static KArgs make_kargs(rr_ctx* c, const rr_render_args* a, uint32_t mask, int l
   K.t6_centroid = (a->flags & RR_T6_TOWARD_LIGHT) ? c->emit_centroid.p : nullptr;
   K.n_centroid = (int)c->emit_centroid.n;
   K.tobj = (a->flags & RR_TOBJ_MIDPATH) ? 1 : 0;
+  K.recon_bidir = (a->flags & RR_RECONNECT_BIDIR) ? 1 : 0;
   K.reconnect = (a->flags & RR_RECONNECT) ? 1 : 0;
   K.reject_multi = (a->flags & RR_REJECT_MULTI) ? 1 : 0;
   K.seed = a->seed;

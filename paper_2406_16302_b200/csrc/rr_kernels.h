@@ -35,6 +35,7 @@ struct KArgs {
   const float4* t6_centroid;         // RR_T6_TOWARD_LIGHT: emitter centroids (world), else null
   int n_centroid;
   int tobj;                          // RR_TOBJ_MIDPATH (variants instantiation)
+  int recon_bidir;                   // RR_RECONNECT_BIDIR (variants instantiation)
   uint64_t i_begin;
   rr_path_record* recs;
   unsigned long long* rec_count;

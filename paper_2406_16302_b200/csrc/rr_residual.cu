@@ -590,12 +590,23 @@ struct BPath {
   float3 dir0, dir1;
   int q0, q1, qyz;
   BSide A, B;  // A: sensor side (slots t), B: emitter side (slots 16 + s)
+#if RR_VAR_KERNELS
+  bool follow;  // RR_RECONNECT_BIDIR: this (mapped) path's emitter side is the base's from the reconnection on
+#endif
 };
 struct BState {
   uint64_t i;
   Rng rng;
   int pc, nmax;
   BPath P, Q;
+#if RR_VAR_KERNELS
+  // RR_RECONNECT_BIDIR (reading 19): rb 0 searching, 1 reconnected (edge visibility pending), 2
+  // reconnected, 3 failed (rb_reason), 4 no reconnection possible; wb the walk-B index; suffix rejection from
+  // rb_from; pending queries q_rb (reconnection edge), q_sfx (suffix edge against dyn_Fbar)
+  int rb, wb, rb_reason, rb_from, sfx_reason, q_rb, q_sfx, sfx_j;
+  bool divb, okPb, okQb;
+  float R1, R2;
+#endif
 };
 
 __device__ void bidir_start_issue(const DevScene& S, const KArgs& A, int tech, int F, const Rng& rng, BPath& G, Batch& B,
@@ -605,6 +616,9 @@ __device__ void bidir_start_issue(const DevScene& S, const KArgs& A, int tech, i
   G.A.n = G.B.n = G.A.nconn = G.B.nconn = 0;
   G.A.ended = G.B.ended = false;
   G.A.qw = G.B.qw = G.A.qc = G.B.qc = -1;
+#if RR_VAR_KERNELS
+  G.follow = false;
+#endif
   if (skip) return;  // the mapped path of RR_NO_PATH_MAPPING: none
   const int D = A.max_depth;
   float d0[8];
@@ -704,6 +718,9 @@ __device__ void bidir_issue(const DevScene& S, const KArgs& A, int tech, int F, 
         W.qc = B.push(mk_seg(v.p, Lt.p, v.tri, Lt.tri, bit(F)));
       }
     }
+#if RR_VAR_KERNELS
+    if (side == 1 && G.follow) continue;  // the emitter side follows the base walk (no rays of its own)
+#endif
     if (!W.ended && W.n < nmax) {
       int m = W.n;
       float d[8];
@@ -820,6 +837,17 @@ __device__ __noinline__ void bidir_finish(const DevScene& S, const KArgs& A, BSt
       }
       if (pc) {
         int stt = qc_ ? ST_ACCEPTED : ST_UNPAIRED, rs = RJ_NONE;
+        float R = 1.0f;
+#if RR_VAR_KERNELS
+        if (A.recon_bidir && st.rb >= 1 && st.rb <= 3 && s >= st.wb + 1) {  // reconnected emitter side
+          if (st.rb == 3) { stt = ST_REJECTED; rs = st.rb_reason; }
+          else if (s >= st.rb_from) { stt = ST_REJECTED; rs = st.sfx_reason; }
+          else if (stt == ST_ACCEPTED) {
+            R = st.R1 * (s >= st.wb + 2 ? st.R2 : 1.0f);
+            if (!(R > 0.0f) || !isfinite(R)) { stt = ST_REJECTED; rs = RJ_TARGET; }
+          }
+        }
+#endif
         if (stt == ST_ACCEPTED && A.reject_multi) {
           bool dv = sdiff;
           int dp = (l == 3) ? 1 : 0, dq = dp;
@@ -834,13 +862,87 @@ __device__ __noinline__ void bidir_finish(const DevScene& S, const KArgs& A, BSt
           }
           if (dv && (dp >= 2 || dq >= 2)) { stt = ST_REJECTED; rs = RJ_MULTI; }
         }
-        finish(o, st.i, 3, t, s, stt, rs, pixp, vp, pixq, vq, 1.0f);
+        finish(o, st.i, 3, t, s, stt, rs, pixp, vp, pixq, vq, R);
       } else {
         finish(o, st.i, 3, t, s, ST_MAPPED_ONLY, RJ_NONE, -1, f3(0.f, 0.f, 0.f), pixq, vq, 1.0f);
       }
     }
   }
 }
+
+#if RR_VAR_KERNELS
+// RR_RECONNECT_BIDIR (P:L387-411 inside the two-ended techniques; reading 19): after the round that
+// extended both emitter sides from index m (lockstep), decide the reconnection at m exactly as the single walks do
+// -- the first index where the pair is diverged (a different vertex, or different directions sampled at a shared
+// one) and both vertices are rough reconnects Q's y'_m to the base's y_{m+1} -- then let Q's emitter side follow
+// the base's: copied vertices, its own NEE connections, each later edge re-checked against dyn_Fbar only.
+__device__ void bidir_recon_step(const DevScene& S, const KArgs& A, BState& st, const Batch& B, int m_before_p,
+                                 int m_before_q) {
+  const int F = A.side, Fb = 1 - F;
+  BPath& P = st.P;
+  BPath& Q = st.Q;
+  if (st.q_rb >= 0) {  // the reconnection edge y'_w -> y_{w+1} in View_Fbar
+    const QRes& r = B.r[st.q_rb];
+    if (r.ok[Fb]) { st.rb = 2; Q.B.ex[st.wb + 1] = r.c[Fb]; }
+    else { st.rb = 3; st.rb_reason = RJ_OCCLUDED; }
+  }
+  if (st.q_sfx >= 0) {  // a shared suffix edge against dyn_Fbar only
+    const QRes& r = B.r[st.q_sfx];
+    if (!r.ok[Fb] && st.sfx_j < st.rb_from) { st.rb_from = st.sfx_j; st.sfx_reason = RJ_OCCLUDED; }
+    Q.B.ex[st.sfx_j] = r.c[Fb];
+  }
+  st.q_rb = st.q_sfx = -1;
+  if (st.rb == 1 || st.rb == 2) {  // follow: copy the base's newest emitter-side vertex
+    if (P.B.n > Q.B.n) {
+      const int j = P.B.n;
+      Q.B.v[j] = P.B.v[j];
+      Q.B.n = j;
+      st.sfx_j = j;  // edge (y_{j-1}, y_j) to re-check with the next batch
+      if (edited(S, P.B.v[j].obj) && j < st.rb_from) { st.rb_from = j; st.sfx_reason = RJ_SUFFIX_DYN; }
+      if (j == st.wb + 2) st.R2 = area_pdf(S, Fb, Q.B.v[st.wb], P.B.v[j - 1], P.B.v[j]) /
+                                  area_pdf(S, F, P.B.v[st.wb], P.B.v[j - 1], P.B.v[j]);
+    } else {
+      st.sfx_j = 0;
+    }
+    Q.B.ended = P.B.ended;
+    return;
+  }
+  if (st.rb != 0) return;
+  // search at index m = the vertex both emitter sides stood on before this round's walk step
+  const int m = m_before_p;
+  if (m < 1 || m != m_before_q) { if (m >= 1) st.rb = 4; return; }
+  st.divb = st.divb || !same_pv(S, P.B.v[m], Q.B.v[m]);
+  const bool dirdiv = (st.okPb != st.okQb) || (st.okPb && st.okQb && !eq3(P.B.wd, Q.B.wd));
+  const Mat mp = load_mat(S, (uint32_t)P.B.v[m].obj, F), mq = load_mat(S, (uint32_t)Q.B.v[m].obj, Fb);
+  if ((st.divb || dirdiv) && rough_enough(mp, A.alpha_min) && rough_enough(mq, A.alpha_min)) {
+    st.wb = m;
+    if (P.B.n < m + 1) { st.rb = 4; return; }  // no target: the base has no connection beyond m
+    const PV& vw = P.B.v[m];
+    const PV& vq = Q.B.v[m];
+    const PV& tg = P.B.v[m + 1];
+    float3 a = sub3(vq.p, tg.p), b = sub3(vw.p, tg.p);
+    float la2 = dot3(a, a), lb2 = dot3(b, b);
+    int rs = RJ_NONE;
+    if (edited(S, tg.obj)) rs = RJ_TARGET;
+    else if (!rough_enough(load_mat(S, (uint32_t)tg.obj, F), A.alpha_min)) rs = RJ_TARGET;
+    else if (fminf(sqrtf(lb2), sqrtf(la2)) < A.dmin) rs = RJ_TARGET;
+    else {
+      float Jg = fabsf(dot3(tg.n, a * (1.0f / sqrtf(la2)))) / fabsf(dot3(tg.n, b * (1.0f / sqrtf(lb2)))) * lb2 / la2;
+      if (!(Jg <= A.jacobian_max && Jg >= 1.0f / A.jacobian_max)) rs = RJ_JACOBIAN;
+    }
+    if (rs != RJ_NONE) { st.rb = 3; st.rb_reason = rs; return; }
+    st.R1 = area_pdf(S, Fb, Q.B.v[m - 1], vq, tg) / area_pdf(S, F, P.B.v[m - 1], vw, tg);
+    st.rb = 1;
+    Q.B.v[m + 1] = tg;  // Q's own hit at m + 1 (if any) is dropped; its emitter side follows the base's
+    Q.B.n = m + 1;
+    Q.B.ended = P.B.ended;
+    Q.follow = true;
+    st.sfx_j = 0;
+    return;
+  }
+  if (dirdiv) st.divb = true;
+}
+#endif
 
 __device__ bool bidir_step(const DevScene& S, const KArgs& A, BState& st, Batch& B, Out& o) {
   const int F = A.side, Fb = 1 - F, l = A.tech;
@@ -861,15 +963,45 @@ __device__ bool bidir_step(const DevScene& S, const KArgs& A, BState& st, Batch&
       B.n = 0;
       bidir_issue(S, A, l, F, st.rng, st.nmax, st.P, B, true);
       bidir_issue(S, A, l, Fb, st.rng, st.nmax, st.Q, B, true);
+#if RR_VAR_KERNELS
+      st.rb = 0;
+      st.wb = 0;
+      st.rb_reason = st.sfx_reason = RJ_NONE;
+      st.rb_from = 1 << 30;
+      st.q_rb = st.q_sfx = -1;
+      st.sfx_j = 0;
+      st.R1 = st.R2 = 1.0f;
+      st.divb = st.P.ok && st.Q.ok && !same_pv(S, st.P.B.v[0], st.Q.B.v[0]);
+      st.okPb = st.P.B.qw >= 0;
+      st.okQb = st.Q.B.qw >= 0;
+#endif
       st.pc = 2;
       if (B.n > 0) return true;
       continue;
     }
+#if RR_VAR_KERNELS
+    const int mbp = st.P.B.n, mbq = st.Q.B.n;  // emitter-side index before this round's walk step
+#endif
     bidir_consume(S, A, F, st.P, B);
     bidir_consume(S, A, Fb, st.Q, B);
+#if RR_VAR_KERNELS
+    if (A.recon_bidir && st.P.ok && st.Q.ok) bidir_recon_step(S, A, st, B, mbp, mbq);
+#endif
     B.n = 0;
     bidir_issue(S, A, l, F, st.rng, st.nmax, st.P, B, false);
     bidir_issue(S, A, l, Fb, st.rng, st.nmax, st.Q, B, false);
+#if RR_VAR_KERNELS
+    if (A.recon_bidir && st.P.ok && st.Q.ok) {
+      st.okPb = st.P.B.qw >= 0;  // a direction was sampled at the emitter side's newest vertex
+      st.okQb = st.Q.B.qw >= 0;
+      if (st.rb == 1)
+        st.q_rb = B.push(mk_seg(st.Q.B.v[st.wb].p, st.Q.B.v[st.wb + 1].p, st.Q.B.v[st.wb].tri,
+                                st.Q.B.v[st.wb + 1].tri, bit(Fb)));
+      if ((st.rb == 1 || st.rb == 2) && st.sfx_j > st.wb + 1)
+        st.q_sfx = B.push(mk_seg(st.Q.B.v[st.sfx_j - 1].p, st.Q.B.v[st.sfx_j].p, st.Q.B.v[st.sfx_j - 1].tri,
+                                 st.Q.B.v[st.sfx_j].tri, bit(Fb), true));
+    }
+#endif
     if (B.n > 0) return true;
     bidir_finish(S, A, st, o);
     return false;
@@ -1125,7 +1257,7 @@ int residual_grid(bool bidir, uint64_t n) {
 }
 int residual_block() { return RR_BLOCK; }
 void launch_residual(const DevScene& S, const KArgs& A, int grid, cudaStream_t st) {
-  if (A.t6_centroid || A.tobj) launch_residual_var(S, A, grid, st);  // SURVEY 8(f) row 4 variants: their own kernels
+  if (A.t6_centroid || A.tobj || A.recon_bidir) launch_residual_var(S, A, grid, st);  // SURVEY 8(f) row 4 variants
   else if (A.mat_type_vndf) launch_residual_vndf(S, A, grid, st);  // RR_VNDF: the other instantiation
   else kplain::launch_kernels(S, A, grid, st);
 }

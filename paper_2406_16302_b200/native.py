@@ -19,6 +19,7 @@ RR_PRIMAL_SHARED_STREAMS = 128  # rr_render_primal: one stream for both states
 RR_NO_PATH_MAPPING = 256  # "incremental w/o PM" ablation (include/rr.h)
 RR_T6_TOWARD_LIGHT = 512  # T6 directions toward the light (include/rr.h)
 RR_TOBJ_MIDPATH = 1024  # object transform of the first mid-path moved-object hit (include/rr.h)
+RR_RECONNECT_BIDIR = 2048  # reconnection inside the T3 / T6 emitter-side sub-walk (include/rr.h)
 
 
 class rr_material(C.Structure):

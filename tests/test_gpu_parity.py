@@ -341,6 +341,22 @@ def test_records_tobj_midpath(torch_cuda, cfg, flags):
         record_parity(w, args, n_per=1024, strided=True)
 
 
+@pytest.mark.parametrize("cfg,flags", [("c1", S.PAPER_FLAGS), ("c1d6", S.PAPER_FLAGS), ("rev", S.PAPER_FLAGS),
+                                       ("c2", S.PAPER_FLAGS), ("c1d6", S.PAPER_FLAGS | S.T6_TOWARD_LIGHT | S.TOBJ_MIDPATH),
+                                       (3, S.PAPER_FLAGS), (4, S.PAPER_FLAGS), (5, S.PAPER_FLAGS)])
+def test_records_reconnect_bidir(torch_cuda, cfg, flags):
+    """RR_RECONNECT_BIDIR (P:L387-411 inside T3 / T6): the emitter-side sub-walk reconnects at its
+    first diverged rough vertex (variants instantiation)."""
+    w = {"c1": S.config1, "c1d6": lambda: S.config1(32, 32, spp=4, max_depth=6),
+         "rev": lambda: S.occluder_reveal(32, 32, spp=8, max_depth=5),
+         "c2": lambda: S.config2(64, 64, spp=8)}.get(cfg, lambda: S.load_config(cfg))()
+    args = dataclasses.replace(w.args, flags=flags | S.RECONNECT_BIDIR)
+    if isinstance(cfg, str):
+        record_parity(w, args, techniques=(3, 6, 7))
+    else:
+        record_parity(w, args, n_per=1024, strided=True, techniques=(3, 6))
+
+
 @pytest.mark.parametrize("cfg", [1, 2, 4])
 def test_records_no_path_mapping(torch_cuda, cfg):
     """RR_NO_PATH_MAPPING ("incremental w/o PM"): every connection unpaired, static paths rejected."""
@@ -500,10 +516,11 @@ def test_invalid_arguments_are_refused(torch_cuda):
     w = S.config1(16, 16)
     r = _renderer(w)
     for bad in (dict(technique_mask=0x3F), dict(spp=3), dict(max_depth=0), dict(max_depth=11),
-                dict(flags=S.RECONNECT), dict(layer_mask=0x80), dict(flags=S.PAPER_FLAGS | 2048),
+                dict(flags=S.RECONNECT), dict(layer_mask=0x80), dict(flags=S.PAPER_FLAGS | 4096),
                 dict(flags=S.PAPER_FLAGS | S.DIAG_ONE_WAY), dict(flags=S.PAPER_FLAGS | S.NO_PATH_MAPPING),
                 dict(flags=S.NO_PATH_MAPPING), dict(flags=S.PAPER_FLAGS | S.VNDF | S.T6_TOWARD_LIGHT),
-                dict(flags=S.TOBJ_MIDPATH), dict(flags=S.PAPER_FLAGS | S.VNDF | S.TOBJ_MIDPATH)):
+                dict(flags=S.TOBJ_MIDPATH), dict(flags=S.PAPER_FLAGS | S.VNDF | S.TOBJ_MIDPATH),
+                dict(flags=S.TWO_WAY | S.RECONNECT_BIDIR)):
         with pytest.raises(RRError):
             r.render_residual(dataclasses.replace(w.args, **bad))
     for bad in (dict(state=2), dict(spp=0), dict(max_depth=0), dict(max_depth=11)):
