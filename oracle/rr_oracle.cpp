@@ -1624,8 +1624,10 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
             sq.tri = gq.start.tri;
           }
           eq = eval_path(cx, Fb, q, true, &sq);
-          const int k = (int)q.x.size();
-          for (int e = 1; e < k - 2; ++e)  // every walk edge of q (the two connection edges only zero V)
+          // the reconnection edge (y'_w, y_{w+1}) and every later walk edge of q must be unoccluded in View_Fbar
+          // (C7); other edges only zero V (f = 0), the connection edges included
+          const int k = (int)q.x.size(), er = t + (l == 3 ? 1 : 0) + wB;
+          for (int e = er; e < k - 2; ++e)
             if (!eq.edge_vis[e]) { status = ST_REJECTED; reason = RJ_OCCLUDED; }
           if (status == ST_ACCEPTED) {
             R = reconnect_R(S, F, gp.B, gq.B, wB, sb);

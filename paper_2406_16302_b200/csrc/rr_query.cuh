@@ -41,11 +41,12 @@ struct __align__(16) Query {
   uint8_t type, want;    // want: bit F set -> evaluate state F
   uint8_t dyn_only;
   uint8_t rev;           // RR_T6_TOWARD_LIGHT kernels: the path runs this edge against the query's direction
-  // x_G of a T4 / T5 / T6 sample on this ray / segment (reading 12): seed_t > 0 its distance, eb its
-  // ghost triangle.  The ghost-crossing jobs skip that crossing (a hit of triangle eb, or within dedup_tol of
-  // seed_t); the consumer adds it exactly (add_seed), so it counts once whether or not the non-watertight
-  // triangle test finds it.  seed_t = 0: none.  (For QT_SEG eb is otherwise the excluded end triangle.)
+  // x_G of a T4 / T5 / T6 sample on this ray / segment (reading 12): seed_t > 0 its distance,
+  // seed_tri its ghost triangle.  The ghost-crossing jobs skip that crossing (a hit of triangle seed_tri, or within
+  // dedup_tol of seed_t); the consumer adds it exactly (add_seed), so it counts once whether or not the
+  // non-watertight triangle test finds it.  seed_t = 0: none.
   float seed_t;
+  int seed_tri;
 };
 
 struct __align__(16) QRes {
@@ -224,7 +225,7 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
     WRay wr = make_wray(o, d);
     traverse<COUNT>(S, root, wr, tmin, tmax, [&](int li, float t, float tm, int id) -> float {
       if (kind == 2) {  // ghost crossing (all hits, dedup within dedup_tol)
-        if (fabsf(t - q.seed_t) < S.dedup_tol || (id == q.eb && q.seed_t > 0.0f)) return tm;  // x_G: added exactly
+        if (fabsf(t - q.seed_t) < S.dedup_tol || (id == q.seed_tri && q.seed_t > 0.0f)) return tm;  // x_G: added exactly
         for (int a = 0; a < ns; ++a)
           if (fabsf(seen[a] - t) < S.dedup_tol) return tm;
         seen[ns < 8 ? ns++ : 7] = t;  // beyond 8 crossings: dedup against the first 7 and the latest one
@@ -290,6 +291,7 @@ __device__ __forceinline__ Query mk_ray(P3 o, float3 d, int excl, int want) {
   q.rev = 0;
 #endif
   q.seed_t = 0.0f;
+  q.seed_tri = -1;
   return q;
 }
 __device__ __forceinline__ Query mk_seg(P3 a, P3 b, int ea, int eb, int want, bool dyn_only = false) {
@@ -308,6 +310,7 @@ __device__ __forceinline__ Query mk_seg(P3 a, P3 b, int ea, int eb, int want, bo
   q.rev = 0;
 #endif
   q.seed_t = 0.0f;
+  q.seed_tri = -1;
   return q;
 }
 // the crossing at x_G (distance t along an edge of length L, 1/|cos_G| = ic) added to an edge's crossing sums

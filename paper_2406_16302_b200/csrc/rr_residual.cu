@@ -128,7 +128,7 @@ __device__ __forceinline__ bool nee_ok(int tech, int m) { return tech == 2 ? m >
 // the sample's own ghost crossing on the queried edge (Query::seed_t; reading 12)
 __device__ __forceinline__ Query seeded(Query q, float t, const PV& xg) {
   q.seed_t = t;
-  q.eb = xg.tri;
+  q.seed_tri = xg.tri;
   return q;
 }
 
@@ -589,6 +589,7 @@ struct BPath {
   PV start;
   float3 dir0, dir1;
   int q0, q1, qyz;
+  bool jvis;   // T6: the edge (z_1, y_1) through x_G is unoccluded in View_F (else every path has f = 0)
   BSide A, B;  // A: sensor side (slots t), B: emitter side (slots 16 + s)
 #if RR_VAR_KERNELS
   bool follow;  // RR_RECONNECT_BIDIR: this (mapped) path's emitter side is the base's from the reconnection on
@@ -612,6 +613,7 @@ struct BState {
 __device__ void bidir_start_issue(const DevScene& S, const KArgs& A, int tech, int F, const Rng& rng, BPath& G, Batch& B,
                                   bool skip = false) {
   G.ok = false;
+  G.jvis = true;
   G.q0 = G.q1 = G.qyz = -1;
   G.A.n = G.B.n = G.A.nconn = G.B.nconn = 0;
   G.A.ended = G.B.ended = false;
@@ -694,7 +696,9 @@ __device__ void bidir_issue(const DevScene& S, const KArgs& A, int tech, int F, 
   G.A.qw = G.B.qw = G.A.qc = G.B.qc = -1;
   if (!G.ok) return;
   if (first && tech == 6 && S.n_moved > 0) {  // crossings of the whole edge y_1 -> z_1, x_G among them
-    Query q = mk_seg(G.A.v[0].p, G.A.v[1].p, -2, -2, bit(F));
+    // its visibility too: the edge must be unoccluded in View_F like every edge of a path (Eq.2 V) -- it is not,
+    // e.g., when x_G also lies on the real object's surface (coplanar faces of a horizontal move)
+    Query q = mk_seg(G.A.v[0].p, G.A.v[1].p, G.A.v[0].tri, G.A.v[1].tri, bit(F));
     G.qyz = B.push(RR_ORIENT(seeded(q, norm3f(sub3(G.start.p, G.A.v[0].p)), G.start), true));
   }
   PV E = cam_pv(S);
@@ -747,6 +751,7 @@ __device__ void bidir_consume(const DevScene& S, const KArgs& A, int F, BPath& G
 #endif
     G.A.ex[1] = add_seed(B.r[G.qyz].c[F], norm3f(sub3(G.start.p, G.A.v[0].p)), L,
                          L / fabsf(dot3(G.start.n, dv)) * pd);
+    G.jvis = B.r[G.qyz].ok[F] != 0;
     G.B.ex[1] = swapc(G.A.ex[1]);
   }
   for (int side = 0; side < 2; ++side) {
@@ -823,14 +828,14 @@ __device__ __noinline__ void bidir_finish(const DevScene& S, const KArgs& A, BSt
       int pixp = -1, pixq = -1;
       if (pc) {
         pixp = project(S, P.A.v[t].p);
-        if (P.A.vis[t] && P.B.vis[s]) {
+        if (P.A.vis[t] && P.B.vis[s] && P.jvis) {
           int k = bidir_path(P, l, t, s, S, st.rng, x, ce);
           vp = path_value(S, x, ce, k, F, A.mask);
         }
       }
       if (qc_) {
         pixq = project(S, Q.A.v[t].p);
-        if (Q.A.vis[t] && Q.B.vis[s]) {
+        if (Q.A.vis[t] && Q.B.vis[s] && Q.jvis) {
           int k = bidir_path(Q, l, t, s, S, st.rng, x, ce);
           vq = path_value(S, x, ce, k, Fb, A.mask);
         }

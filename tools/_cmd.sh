@@ -1,3 +1,2 @@
-bash tools/gpu_tests.sh
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 900 python bench.py --impl reference --steps 3 --warmup 1 2>&1 | tail -1
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
+timeout 1500 python -m pytest tests -m gpu -q -k "reconnect_bidir or invalid" > gpurun_out/pt.log 2>&1; echo "pytest $?"; tail -5 gpurun_out/pt.log; grep -E "^E .*Assert" gpurun_out/pt.log | cut -c1-900 | head -8
