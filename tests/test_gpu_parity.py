@@ -67,7 +67,9 @@ def compare_records(grecs, orecs):
         # a pixel only matters where its term is nonzero (contribution-free records splat nothing)
         pix_ok = ((g.pix_p == o.pix_p or not (np.any(np.abs(gp) > TINY) or np.any(np.abs(o.term_p) > TINY))) and
                   (g.pix_q == o.pix_q or not (np.any(np.abs(gq) > TINY) or np.any(np.abs(o.term_q) > TINY))))
-        same = (g.status == o.status and pix_ok and
+        # ... and so does the status (the weights it selects multiply zero); reading 7
+        zero = not any(np.any(np.abs(np.asarray(x, np.float64)) > TINY) for x in (gp, gq, o.term_p, o.term_q))
+        same = ((g.status == o.status or zero) and pix_ok and
                 _close(np.array(g.term_p, np.float64), np.array(o.term_p)) and
                 _close(np.array(g.term_q, np.float64), np.array(o.term_q)))
         if same:
