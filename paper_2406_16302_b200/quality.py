@@ -10,7 +10,9 @@ ablations of the method:
                           dynamic techniques separately, no path mapping (RR_NO_PATH_MAPPING);
   * "residual_replay"  -- two-way, no reconnection: diverged paths are replayed only (RR_RECONNECT off);
   * "residual_one_way" -- one side per technique, replay only (flags 0; SPEC's "mapping off" run knob);
-  * "residual_vndf"    -- the paper's mode with GGX visible-normal sampling (RR_VNDF).
+  * "residual_vndf"    -- the paper's mode with GGX visible-normal sampling (RR_VNDF; SURVEY 8(f) row 4);
+  * "residual_t6_light", "residual_tobj", "residual_recon_bidir", "residual_variants" -- the paper's mode with
+                          RR_T6_TOWARD_LIGHT, RR_TOBJ_MIDPATH, RR_RECONNECT_BIDIR, and all three (row 4).
 
 The reference is NOT any of these estimators: it is the GPU primal renderer (unidirectional NEE/BSDF-MIS path
 tracing, rr_primal.cu, checked against the CPU reference's primal renderer by the tests) run in both states with the SAME random numbers
@@ -81,6 +83,11 @@ def estimators(r, args, spp: int, seed: int = 0, ablations: bool = False) -> Dic
         out["residual_one_way"] = _timed(lambda: r.render_residual(one).clone())
         vn = dataclasses.replace(full, seed=seed + 17, flags=PAPER_FLAGS | 32)
         out["residual_vndf"] = _timed(lambda: r.render_residual(vn).clone())
+        # the other SURVEY 8(f) row 4 variants (each alone and all three together)
+        for name, f in (("residual_t6_light", 512), ("residual_tobj", 1024), ("residual_recon_bidir", 2048),
+                        ("residual_variants", 512 | 1024 | 2048)):
+            va = dataclasses.replace(full, seed=seed + 19, flags=PAPER_FLAGS | f)
+            out[name] = _timed(lambda: r.render_residual(va).clone())
     return out
 
 
