@@ -13,12 +13,21 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named ranges of the host API calls in Nsight timelines
+
 #include "../../include/rr.h"
 #include "rr_device.cuh"
 #include "rr_internal.h"
 #include "rr_kernels.h"
 
 using namespace rr;
+
+namespace {
+struct NvtxRange {  // RAII range around one ABI call
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 struct rr_ctx {
   int device = 0;
@@ -146,6 +155,7 @@ void rr_destroy(rr_ctx* c) {
 const char* rr_last_error(const rr_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 rr_status rr_scene_upload(rr_ctx* c, const rr_scene_desc* d) {
+  NvtxRange nvtx_("rr_scene_upload");
   if (!c || !d) return fail(c, RR_E_INVALID, "null argument");
   if (!d->positions || !d->indices || !d->tri_object || !d->objects || !d->materials)
     return fail(c, RR_E_INVALID, "null array in scene description");
@@ -545,6 +555,7 @@ rr_status rr_scene_upload(rr_ctx* c, const rr_scene_desc* d) {
 }
 
 rr_status rr_set_edit(rr_ctx* c, uint32_t n, const rr_edit* edits) {
+  NvtxRange nvtx_("rr_set_edit");
   if (!c) return RR_E_INVALID;
   if (!c->have_scene) return fail(c, RR_E_STATE, "set_edit before scene upload");
   if (n && !edits) return fail(c, RR_E_INVALID, "null edit list");
@@ -801,6 +812,7 @@ static KArgs make_kargs(rr_ctx* c, const rr_render_args* a, uint32_t mask, int l
 static int prepare_launch(rr_ctx*, KArgs& K) { return residual_grid(K.tech == 3 || K.tech == 6, K.n_local); }
 
 rr_status rr_render_residual(rr_ctx* c, const rr_render_args* a, float* d_image, uint64_t stream) {
+  NvtxRange nvtx_("rr_render_residual");
   if (!c) return RR_E_INVALID;
   if (!c->have_scene) return fail(c, RR_E_STATE, "render before scene upload");
   if (!d_image) return fail(c, RR_E_INVALID, "null image");
@@ -840,6 +852,7 @@ rr_status rr_render_residual(rr_ctx* c, const rr_render_args* a, float* d_image,
 
 rr_status rr_render_primal(rr_ctx* c, uint32_t state, uint32_t spp, uint64_t seed, uint32_t max_depth, uint32_t flags,
                            float* d_image, uint64_t stream) {
+  NvtxRange nvtx_("rr_render_primal");
   if (!c) return RR_E_INVALID;
   if (!c->have_scene) return fail(c, RR_E_STATE, "render before scene upload");
   if (!d_image || spp == 0 || state > 1 || max_depth < 1 || max_depth > RR_MAX_DEPTH)

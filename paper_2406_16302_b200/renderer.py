@@ -163,18 +163,47 @@ class Renderer:
                 out[l] = self.render_residual(dataclasses.replace(args, layer_mask=1 << (l - 1))).clone()
         return out
 
-    def render_sequence(self, frames, args, image=None, shard_index: int = 0, shard_count: int = 1):
+    def render_sequence(self, frames, args, image=None, shard_index: int = 0, shard_count: int = 1,
+                        checkpoint_dir: Optional[str] = None, start_frame: int = 0):
         """Chained residuals of an animation (config 5): frame f applies the edit S_f -> S_f+1
         (`frames[f]`, a list of edits), renders its residual with seed args.seed + f and adds it to `image`,
-        so that after the last frame image = I_0 + sum_f Delta_f (I_0 = the given image, else 0)."""
+        so that after the last frame image = I_0 + sum_f Delta_f (I_0 = the given image, else 0).
+        checkpoint_dir: after every frame the accumulated image is written there as `chain_fNNN.pfm` (float32,
+        exact) with `chain_state.json` naming the last finished frame; `resume_sequence` continues from it.
+        start_frame: the first frame to render (the frames before it are already in `image`)."""
         import dataclasses
-        for f, edits in enumerate(frames):
-            self.set_edit(edits)
+        import json
+        import os
+        for f in range(start_frame, len(frames)):
+            self.set_edit(frames[f])
             a = dataclasses.replace(args, seed=int(args.seed) + f)
             acc = image is not None
             image = self.render_residual(a, image=image, shard_index=shard_index, shard_count=shard_count,
                                          accumulate=acc)
+            if checkpoint_dir is not None:
+                from .io import write_pfm
+                os.makedirs(checkpoint_dir, exist_ok=True)
+                path = os.path.join(checkpoint_dir, f"chain_f{f:03d}.pfm")
+                write_pfm(path, image.cpu().numpy())
+                with open(os.path.join(checkpoint_dir, "chain_state.json"), "w") as fh:
+                    json.dump({"frame": f, "image": os.path.basename(path), "frames": len(frames),
+                               "seed": int(args.seed), "shard": [shard_index, shard_count]}, fh)
         return image
+
+    def resume_sequence(self, frames, args, checkpoint_dir: str, shard_index: int = 0, shard_count: int = 1):
+        """Continue an interrupted render_sequence from its last checkpoint (frame-level resume; the image is
+        restored exactly from the float32 PFM, so the result equals an uninterrupted chain)."""
+        import json
+        import os
+        import torch
+        from .io import read_pfm
+        with open(os.path.join(checkpoint_dir, "chain_state.json")) as fh:
+            st = json.load(fh)
+        rgb = read_pfm(os.path.join(checkpoint_dir, st["image"]))
+        img = torch.zeros((self.height, self.width, 4), dtype=torch.float32, device=f"cuda:{self.device}")
+        img[..., :3] = torch.from_numpy(rgb).to(img.device)
+        return self.render_sequence(frames, args, image=img, shard_index=shard_index, shard_count=shard_count,
+                                    checkpoint_dir=checkpoint_dir, start_frame=int(st["frame"]) + 1)
 
     def render_residual_host(self, args, out: Optional[np.ndarray] = None, shard_index: int = 0,
                              shard_count: int = 1) -> np.ndarray:

@@ -378,6 +378,20 @@ def test_records_config5_late_frame(torch_cuda):
     record_parity(w, w.args, n_per=1024, strided=True)
 
 
+def test_config5_chain_checkpoint_resume(torch_cuda, tmp_path):
+    """render_sequence checkpoints every frame (PFM + state); resuming from frame 1 gives the uninterrupted chain
+    bitwise (float32 PFM is exact)."""
+    torch = torch_cuda
+    w = S.config5(64, 36, spp=4, max_depth=4, n_frames=4)
+    r = _renderer(w)
+    full = r.render_sequence(w.frames, w.args).clone()
+    r.render_sequence(w.frames[:2], w.args, checkpoint_dir=str(tmp_path))  # "interrupted" after frame 1
+    resumed = r.resume_sequence(w.frames, w.args, str(tmp_path))
+    torch.cuda.synchronize()
+    assert torch.equal(full, resumed)
+    assert (tmp_path / "chain_f003.pfm").exists()
+
+
 def test_config5_chain_is_sum_of_frames(torch_cuda):
     """render_sequence(frames) = sum of the per-frame residuals (accumulation on the device; fp32 adds)."""
     torch = torch_cuda
