@@ -1485,11 +1485,6 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
     out[1] = zero ? 0.0 : e.f.y / e.Pi;
     out[2] = zero ? 0.0 : e.f.z / e.Pi;
   };
-  // a sensor connection whose vertex projects outside the image has value 0 (reading 4; its splat
-  // would be dropped): the GPU path does not trace such connections
-  auto offscreen_zero = [&](const Conn& c, int pixel, double v[3]) {
-    if (c.key.kind >= 2 && pixel < 0) v[0] = v[1] = v[2] = 0.0;
-  };
   auto count_dyn = [&](const Path& P) {
     int n = 0;
     for (size_t m = 1; m + 1 < P.x.size(); ++m)
@@ -1517,7 +1512,6 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
     Eval ep = eval_path(cx, F, c.path, true, &sp);
     double vp[3];
     value(ep, vp);
-    offscreen_zero(c, c.path.pixel, vp);
     if (nopm && !ep.dynamic) vp[0] = vp[1] = vp[2] = 0.0;
     r.n_cand_p = ep.n_cand;
     for (int ch = 0; ch < 3; ++ch) r.v_p[ch] = vp[ch];
@@ -1658,7 +1652,6 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
     double vq[3] = {0, 0, 0};
     if (have_q) {
       value(eq, vq);
-      offscreen_zero(c, q.pixel, vq);
       r.n_cand_q = eq.n_cand;
       r.pix_q = q.pixel;
     }
@@ -1709,7 +1702,6 @@ void residual_sample(Ctx& cx, const orc_args& A, int l, int side, uint64_t i, do
       Eval eq = eval_path(cx, Fb, c.path, true, &sq);
       double vq[3];
       value(eq, vq);
-      offscreen_zero(c, c.path.pixel, vq);
       orc_record r;
       std::memset(&r, 0, sizeof(r));
       r.tech = l; r.side = side; r.i = i;

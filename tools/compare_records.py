@@ -49,8 +49,10 @@ def compare(name, w, args, n_per, techs=range(1, 8), verbose=5):
         nz = lambda a: bool(np.any(np.abs(np.asarray(a)) > 1e-30))
         pix_ok = ((int(g[8]) == r.pix_p or not (nz(g[9:12]) or nz(r.term_p))) and
                   (int(g[12]) == r.pix_q or not (nz(g[13:16]) or nz(r.term_q))))
-        tp_ok = close(g[9:12], np.array(r.term_p))
-        tq_ok = close(g[13:16], np.array(r.term_q))
+        off_p = int(g[8]) < 0 and r.pix_p < 0  # dropped splats (reading 4)
+        off_q = int(g[12]) < 0 and r.pix_q < 0
+        tp_ok = off_p or close(g[9:12], np.array(r.term_p))
+        tq_ok = off_q or close(g[13:16], np.array(r.term_q))
         if st_ok and pix_ok and tp_ok and tq_ok:
             ok += 1
             continue
