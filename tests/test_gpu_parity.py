@@ -385,7 +385,7 @@ def test_records_config5_late_frame(torch_cuda):
 
 def test_config5_chain_checkpoint_resume(torch_cuda, tmp_path):
     """render_sequence checkpoints every frame (PFM + state); resuming from frame 1 gives the uninterrupted chain
-    bitwise (float32 PFM is exact)."""
+    (the PFM round trip is exact; the float atomics of the splat make two renders differ in the last bits)."""
     torch = torch_cuda
     w = S.config5(64, 36, spp=4, max_depth=4, n_frames=4)
     r = _renderer(w)
@@ -393,7 +393,8 @@ def test_config5_chain_checkpoint_resume(torch_cuda, tmp_path):
     r.render_sequence(w.frames[:2], w.args, checkpoint_dir=str(tmp_path))  # "interrupted" after frame 1
     resumed = r.resume_sequence(w.frames, w.args, str(tmp_path))
     torch.cuda.synchronize()
-    assert torch.equal(full, resumed)
+    scale = float(full.abs().max())
+    assert scale > 0 and float((full - resumed).abs().max()) <= 1e-5 * scale
     assert (tmp_path / "chain_f003.pfm").exists()
 
 
