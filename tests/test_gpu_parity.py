@@ -472,6 +472,25 @@ def test_image_rmse_configs_2_to_5(torch_cuda, key):
     image_parity(torch_cuda, key)
 
 
+@pytest.mark.parametrize("flags", [
+    S.DIAG_ONE_WAY | S.RECONNECT | S.REJECT_MULTI | S.RECONNECT_BIDIR | S.T6_TOWARD_LIGHT | S.TOBJ_MIDPATH,
+    S.TWO_WAY | S.NO_PATH_MAPPING | S.T6_TOWARD_LIGHT,
+    S.PAPER_FLAGS | S.T6_TOWARD_LIGHT | S.TOBJ_MIDPATH | S.RECONNECT_BIDIR,
+    S.TWO_WAY | S.TOBJ_MIDPATH | S.T6_TOWARD_LIGHT])
+def test_flag_combinations_image_parity(torch_cuda, flags):
+    """Combinations of the mapping variants and test modes, image against the oracle (config 1, 32^2, 16 spp)."""
+    torch = torch_cuda
+    w = S.config1(32, 32, spp=16, max_depth=5, seed=3)
+    args = dataclasses.replace(w.args, flags=flags)
+    r = _renderer(w)
+    g = r.render_residual(args)[..., :3].double().cpu().numpy()
+    o = _oracle(w)
+    ref, _, _ = o.render_residual(args)
+    scale = np.abs(ref).max()
+    assert scale > 0
+    assert math.sqrt(((g - ref) ** 2).mean()) <= 1e-3 * scale, flags
+
+
 def test_identity_edit_exact_zero_config4(torch_cuda):
     """The identity edit (old == new transform bitwise, materials equal) of the 2M-triangle scene at full size
     (1024^2, D = 8, all flags): every term cancels bitwise, the image is exactly 0."""
