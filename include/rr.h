@@ -172,7 +172,10 @@ typedef struct {
   uint64_t sched[8];       /* warp-scheduler occupancy of the residual kernels (diagnostics): [0] warp
                               rounds, [2] sample steps, [3] queries per round summed, [4] lanes holding
                               a sample summed over rounds, [5] deepest BVH root-to-leaf path in inner
-                              nodes (scene property; upload fails above RR_STACK = 64), ([1], [6..7] reserved, 0) */
+                              nodes (scene property; upload fails above RR_STACK = 64), [6] / [7] internal nodes fetched
+                              in dynamic-instance / ghost-crossing BLAS jobs (RR_COUNT_TRAVERSAL in a library built with
+                              -DRR_COUNT_JOBS=1, tools/variants.py; else 0), ([1]
+                              reserved, 0) */
   uint64_t r_hist[16];     /* accepted connections of reconnected pairs (R != 1, C7) by floor(log2 R) + 8, clamped to
                               [0, 15]: bin b holds R in [2^(b-8), 2^(b-7)) (SURVEY 8(f) row 3, R statistics) */
 } rr_stats;

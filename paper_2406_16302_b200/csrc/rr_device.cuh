@@ -13,9 +13,6 @@
 #define RR_PI_F 3.14159265358979323846f
 #define RR_INV_PI_F 0.318309886183790671538f
 #define RR_STACK 64
-#ifndef RR_SSTACK
-#define RR_SSTACK 0  // traversal-stack entries kept in shared memory (blocks of 128 threads); 0: all local
-#endif
 #define RR_TMAX 1.0e30f  // every query's tmax is below the 'empty child' sentinel box at 3e38
 
 namespace rr {
@@ -339,8 +336,14 @@ __device__ __forceinline__ void box2(const WRay& r, float4 n0, float4 n1, float4
   t1 = a1;
 }
 
+#ifndef RR_COUNT_JOBS
+#define RR_COUNT_JOBS 0  // 1: diagnostic build (tools/variants.py) that also splits node fetches by BLAS job kind
+#endif
 struct TCount {  // traversal work of one thread: internal nodes fetched, triangles tested (64 B / 48 B each)
   uint32_t nodes, tris;
+#if RR_COUNT_JOBS
+  uint32_t inst_nodes, ghost_nodes;  // of which in dynamic-instance BLAS jobs / ghost-crossing jobs (diagnostic build)
+#endif
 };
 
 

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(RR_PRIMAL_BLOCK, 8) k_primal(const __grid_cons
     rng.dims(0, d);
     float3 dir = camera_dir(S, (float)(pix % S.W) + d[0], (float)(pix / S.W) + d[1]);
     QRes r;
-    run_query<COUNT>(S, mk_ray(E.p, dir, -1, 1 << F), r, qc);
+    run_query<COUNT, true>(S, mk_ray(E.p, dir, -1, (1 << F) | QW_NO_CROSS), r, qc);
     if (!r.ok[F]) continue;
     PV prev = E, cur = hit_pv(S, r.h[F], E.p, dir, F);
     float3 thr = f3(1.f, 1.f, 1.f), L = f3(0.f, 0.f, 0.f);  // W_e G / p_cam = 1
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(RR_PRIMAL_BLOCK, 8) k_primal(const __grid_cons
         float3 wl = dl * (1.0f / sqrtf(d2));
         float3 Le = emitted(S, xl, cur.p);
         if (nonzero3(Le)) {
-          run_query<COUNT>(S, mk_seg(cur.p, xl.p, cur.tri, xl.tri, 1 << F), r, qc);
+          run_query<COUNT, true>(S, mk_seg(cur.p, xl.p, cur.tri, xl.tri, (1 << F) | QW_NO_CROSS), r, qc);
           if (r.ok[F]) {
             float3 fr = bsdf_eval(mt, cur.n, wi, wl);
             float cosl = fabsf(dot3(xl.n, wl));
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(RR_PRIMAL_BLOCK, 8) k_primal(const __grid_cons
       if (!(pw > 0.0f)) break;
       float3 fr = bsdf_eval(mt, cur.n, wi, wo);
       thr = mul3(thr, fr) * (fabsf(dot3(cur.n, wo)) / pw);
-      run_query<COUNT>(S, mk_ray(cur.p, wo, cur.tri, 1 << F), r, qc);
+      run_query<COUNT, true>(S, mk_ray(cur.p, wo, cur.tri, (1 << F) | QW_NO_CROSS), r, qc);
       if (!r.ok[F]) break;
       prev = cur;
       cur = hit_pv(S, r.h[F], prev.p, wo, F);

@@ -1,10 +1,11 @@
 // rr_query.cuh -- the one generic ray query of the residual kernels.
 //
-// Every traversal of the estimator goes through run_query(), which contains the library's ONLY traversal
-// loop (traverse()): a query is decomposed into BLAS jobs (the static BLAS once, then each dynamic instance
-// under the transform of each requested state, then each MOVED instance under the other state's transform
-// for the ghost crossings), and one traverse() call site serves every job, so lanes that trace queries of
-// different kinds still execute one instruction stream.
+// Every traversal of the residual kernels goes through run_batch() (a lane's whole query batch in one
+// warp-synchronous loop); run_query() (one query, one traverse() per BLAS job) serves the stand-alone trace /
+// segment kernels and the primal renderer.  A query is decomposed into BLAS jobs (the static BLAS once, then
+// each dynamic instance under the transform of each requested state, then each MOVED instance under the other
+// state's transform for the ghost crossings); both loops share the node and triangle steps (node_step,
+// tri_hit), so lanes that trace queries of different kinds execute one instruction stream.
 //
 //
 //  QT_CLOSEST: closest hit of the ray (o, d) in View_F = static + dyn at M_F (ghosts transparent),
@@ -20,6 +21,9 @@
 namespace rr {
 
 enum { QT_CLOSEST = 0, QT_SEG = 1 };
+// Query::want: bit F = evaluate state F; QW_NO_CROSS = the caller does not use this query's ghost crossings (their
+// jobs are skipped; QRes::c stays zero)
+enum { QW_NO_CROSS = 4 };
 // cache policy of the BVH node / leaf-row loads (tuning knob; __ldg = read-only path through L1)
 #ifndef RR_NODE_LD
 #define RR_NODE_LD __ldg
@@ -57,95 +61,154 @@ struct __align__(16) QRes {
 
 // ------------------------------------------------------------------------------------------------
 // BVH2 traversal (64-byte nodes, single-triangle leaves; rr_lbvh.cu): nearer hit child first, the other
-// pushed.  leaf(li, t, tmax, id) is called for every triangle hit with t in (tmin, tmax) and returns the new
-// tmax (negative: terminate).  id = the triangle's global id (stored in the first vertex's w).
+// pushed.
+//
+// Convergence (B200 / independent thread scheduling).  Lanes of a warp that take different branches of a
+// traversal iteration (descend / push / pop / leaf) are merged again only at a convergence barrier; with the
+// barrier after the loop (where the compiler puts it for a plain while loop) every lane runs its whole traversal
+// alone: ncu measured 1.6 active threads per warp instruction on random camera rays in a stand-alone trace kernel
+// (profiles/r2_trace_convergence.md).  The SYNC loop therefore ends each iteration with a __ballot_sync over the
+// lanes still traversing, and a lane that has finished leaves after that ballot (its bit is cleared from the next
+// iteration's mask): the group stays converged, one node (or leaf) per lane per iteration -- same nodes, same
+// results, 372 -> 1193 Mrays/s on config 4 (rr_trace), 8.3 active threads per instruction.  The residual
+// megakernels keep the plain loop (SYNC = false; see traverse()).
 // ------------------------------------------------------------------------------------------------
-template <bool COUNT, class Leaf>
-__device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay& r_in, float tmin, float tmax, Leaf leaf,
+
+// one internal node: both child boxes against (tmin, tmax); descend into the nearer hit child and push the other.
+// Returns true when neither child is hit (the caller pops).
+__device__ __forceinline__ bool node_step(const DevScene& S, const WRay& r, float tmin, float tmax, int& node,
+                                          int* stack, int& sp) {
+  const float4* nd = S.nodes + 4 * node;
+  float4 n0 = RR_NODE_LD(nd), n1 = RR_NODE_LD(nd + 1), n2 = RR_NODE_LD(nd + 2), n3 = RR_NODE_LD(nd + 3);
+  bool h0, h1;
+  float t0, t1;
+  box2(r, n0, n1, n2, tmin, tmax, h0, h1, t0, t1);
+  int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
+  if (h0 && h1) {
+    if (t1 < t0) {
+      int t = c0;
+      c0 = c1;
+      c1 = t;
+    }
+    if (sp < RR_STACK) stack[sp++] = c1;
+    node = c0;
+    return false;
+  }
+  if (h0) {
+    node = c0;
+    return false;
+  }
+  if (h1) {
+    node = c1;
+    return false;
+  }
+  return true;
+}
+
+// leaf triangle li: the unit-triangle test (Woop 2004): plane distance, then barycentrics u, v of the plane point.
+// True for a hit with t in (tmin, tmax).
+__device__ __forceinline__ bool tri_hit(const DevScene& S, const WRay& r, int li, float tmin, float tmax, float& t) {
+  const float4* xp = S.lxf + 3 * li;
+  const float4 m2 = RR_TRI_LD(xp + 2);
+  // explicit FMAs (the library builds with -fmad=false; rounding here is the same for both states)
+  const float oz = fmaf(m2.x, r.o.x, fmaf(m2.y, r.o.y, fmaf(m2.z, r.o.z, m2.w)));
+  const float dz = fmaf(m2.x, r.d.x, fmaf(m2.y, r.d.y, m2.z * r.d.z));
+  t = __fdividef(-oz, dz);  // 2 ulp; the hit point itself is recomputed in fp64 (hit_pv)
+  if (!(t > tmin && t < tmax)) return false;
+  const float4 m0 = RR_TRI_LD(xp);
+  const float u = fmaf(t, fmaf(m0.x, r.d.x, fmaf(m0.y, r.d.y, m0.z * r.d.z)),
+                       fmaf(m0.x, r.o.x, fmaf(m0.y, r.o.y, fmaf(m0.z, r.o.z, m0.w))));
+  if (!(u >= 0.0f && u <= 1.0f)) return false;
+  const float4 m1 = RR_TRI_LD(xp + 1);
+  const float v = fmaf(t, fmaf(m1.x, r.d.x, fmaf(m1.y, r.d.y, m1.z * r.d.z)),
+                       fmaf(m1.x, r.o.x, fmaf(m1.y, r.o.y, fmaf(m1.z, r.o.z, m1.w))));
+  return v >= 0.0f && u + v <= 1.0f;
+}
+
+// One traversal of one BLAS.  leaf(li, t, tmax, id) is called for every triangle hit with t in (tmin, tmax) and
+// returns the new tmax (negative: terminate).  id = the triangle's global id (stored in the first vertex's w).
+// SYNC: the ballot-per-iteration loop (stand-alone kernels, whose lanes enter converged).  The residual
+// megakernels use SYNC = false: there the lanes reach a traversal in small groups (per query slot and BLAS job),
+// and the ballot, the uniform job loop and the extra live registers cost more than the reconvergence returns
+// (config 4: 9.63 s vs 8.42 s, round-2 rejected designs).
+template <bool COUNT, bool SYNC, class Leaf>
+__device__ __forceinline__ void traverse(const DevScene& S, int root, const WRay& r, float tmin, float tmax, Leaf leaf,
                                          TCount& tc) {
-  const WRay& r = r_in;
-#if RR_SSTACK > 0
-  // short stack: the first RR_SSTACK entries in shared memory (entry k of thread t at [k][t], conflict-free),
-  // the rest in local memory
-  __shared__ int sstack[RR_SSTACK][128];
-  int* const sbase = &sstack[0][threadIdx.x];
-  int stack[RR_STACK - RR_SSTACK];
-#else
   int stack[RR_STACK];
-#endif
   int sp = 0;
   int node = root;
   uint32_t nn = 0, nt = 0;
+  if constexpr (!SYNC) {
+    // the residual megakernels' loop, as tuned there (descend with continue, pop at the bottom)
+    while (true) {
+      if (node >= 0) {
+        if (COUNT) nn++;
+        const float4* nd = S.nodes + 4 * node;
+        float4 n0 = RR_NODE_LD(nd), n1 = RR_NODE_LD(nd + 1), n2 = RR_NODE_LD(nd + 2), n3 = RR_NODE_LD(nd + 3);
+        bool h0, h1;
+        float t0, t1;
+        box2(r, n0, n1, n2, tmin, tmax, h0, h1, t0, t1);
+        int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
+        if (h0 && h1) {
+          if (t1 < t0) {
+            int t = c0;
+            c0 = c1;
+            c1 = t;
+          }
+          if (sp < RR_STACK) stack[sp++] = c1;
+          node = c0;
+          continue;
+        } else if (h0) {
+          node = c0;
+          continue;
+        } else if (h1) {
+          node = c1;
+          continue;
+        }
+      } else {
+        int li = ~node;
+        if (COUNT) nt++;
+        float t;
+        if (tri_hit(S, r, li, tmin, tmax, t)) {
+          tmax = leaf(li, t, tmax, __float_as_int(__ldg(S.ltris + 3 * li).w));
+          if (tmax < 0.0f) break;
+        }
+      }
+      if (sp == 0) break;
+      node = stack[--sp];
+    }
+    tc.nodes += nn;
+    tc.tris += nt;
+    return;
+  }
+  unsigned live = __activemask();
+  bool done = false;
   while (true) {
+    bool pop;
     if (node >= 0) {
       if (COUNT) nn++;
-      const float4* nd = S.nodes + 4 * node;
-      float4 n0 = RR_NODE_LD(nd), n1 = RR_NODE_LD(nd + 1), n2 = RR_NODE_LD(nd + 2), n3 = RR_NODE_LD(nd + 3);
-      bool h0, h1;
-      float t0, t1;
-      box2(r, n0, n1, n2, tmin, tmax, h0, h1, t0, t1);
-      int c0 = __float_as_int(n3.x), c1 = __float_as_int(n3.y);
-      if (h0 && h1) {
-        if (t1 < t0) {
-          int t = c0;
-          c0 = c1;
-          c1 = t;
-        }
-#if RR_SSTACK > 0
-        if (sp < RR_SSTACK) sbase[128 * sp++] = c1;
-        else if (sp < RR_STACK) { stack[sp - RR_SSTACK] = c1; sp++; }
-#else
-        if (sp < RR_STACK) stack[sp++] = c1;
-#endif
-        node = c0;
-        continue;
-      } else if (h0) {
-        node = c0;
-        continue;
-      } else if (h1) {
-        node = c1;
-        continue;
-      }
+      pop = node_step(S, r, tmin, tmax, node, stack, sp);
     } else {
-      int li = ~node;
+      const int li = ~node;
       if (COUNT) nt++;
-      // unit-triangle test (Woop 2004): plane distance, then barycentrics u, v of the plane point
-      const float4* xp = S.lxf + 3 * li;
-      const float4 m2 = RR_TRI_LD(xp + 2);
-      // explicit FMAs (the library builds with -fmad=false; rounding here is the same for both states)
-      const float oz = fmaf(m2.x, r.o.x, fmaf(m2.y, r.o.y, fmaf(m2.z, r.o.z, m2.w)));
-      const float dz = fmaf(m2.x, r.d.x, fmaf(m2.y, r.d.y, m2.z * r.d.z));
-      const float t = __fdividef(-oz, dz);  // 2 ulp; the hit point itself is recomputed in fp64 (hit_pv)
-      if (t > tmin && t < tmax) {
-        const float4 m0 = RR_TRI_LD(xp);
-        const float u = fmaf(t, fmaf(m0.x, r.d.x, fmaf(m0.y, r.d.y, m0.z * r.d.z)),
-                             fmaf(m0.x, r.o.x, fmaf(m0.y, r.o.y, fmaf(m0.z, r.o.z, m0.w))));
-        if (u >= 0.0f && u <= 1.0f) {
-          const float4 m1 = RR_TRI_LD(xp + 1);
-          const float v = fmaf(t, fmaf(m1.x, r.d.x, fmaf(m1.y, r.d.y, m1.z * r.d.z)),
-                               fmaf(m1.x, r.o.x, fmaf(m1.y, r.o.y, fmaf(m1.z, r.o.z, m1.w))));
-          if (v >= 0.0f && u + v <= 1.0f) {
-            tmax = leaf(li, t, tmax, __float_as_int(__ldg(S.ltris + 3 * li).w));
-            if (tmax < 0.0f) break;
-          }
-        }
+      pop = true;
+      float t;
+      if (tri_hit(S, r, li, tmin, tmax, t)) {
+        tmax = leaf(li, t, tmax, __float_as_int(__ldg(S.ltris + 3 * li).w));
+        if (tmax < 0.0f) done = true;
       }
     }
-    if (sp == 0) break;
-#if RR_SSTACK > 0
-    --sp;
-    node = sp < RR_SSTACK ? sbase[128 * sp] : stack[sp - RR_SSTACK];
-#else
-    node = stack[--sp];
-#endif
+    if (pop && !done) {
+      if (sp == 0) done = true;
+      else node = stack[--sp];
+    }
+    live = __ballot_sync(live, !done);  // the lanes still traversing: the next iteration's group
+    if (done) break;
   }
   tc.nodes += nn;
   tc.tris += nt;
 }
 
-// COUNT: count node fetches and triangle tests (rr_stats.nodes_visited / tris_tested; off in timed renders,
-// where the two counters cost ~3%).  Inlined into its call site: under the 32-register budget a call boundary
-// forces the scene pointers through generic loads and spills (-9% on config 4 when inlined).
 #if defined(RR_VAR_KERNELS) && RR_VAR_KERNELS
 // RR_T6_TOWARD_LIGHT: 4 pi p_dir(d | x) of T6's direction d at a ghost point x (the oracle's t6_pdir):
 // (2 / n_e) #{e : d . (c_e - x) > 0}; 1 for the uniform sphere
@@ -159,7 +222,7 @@ __device__ __forceinline__ float t6_pdir4pi(const float4* c, int n, float3 x, fl
 }
 #endif
 
-template <bool COUNT>
+template <bool COUNT, bool SYNC>
 __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRes& r, QCount& qc
 #if defined(RR_VAR_KERNELS) && RR_VAR_KERNELS
                                           , const float4* t6c, int t6n
@@ -182,21 +245,32 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
   int ns = 0, seen_state = -1;
   const int NI = S.n_inst;
   const int njobs = 1 + 4 * NI;
+  // SYNC: the job loop is uniform over the calling group (every lane runs every j; a lane that skips job j waits
+  // at the __syncwarp below), so the lanes that do need job j enter traverse() together and stay converged.
+  // Otherwise a skipped job is a plain `continue` (mine stays true).
+  const unsigned grp_mask = SYNC ? __activemask() : 0u;
+#define RR_SKIP_JOB          \
+  {                          \
+    if (SYNC) mine = false;  \
+    else continue;           \
+  }
   for (int j = 0; j < njobs; ++j) {
     int kind, F = 0, k = -1;
+    bool mine = true;
     if (j == 0) {
       kind = 0;
-      if (q.dyn_only || S.static_root < 0) continue;
+      if (q.dyn_only || S.static_root < 0) RR_SKIP_JOB
     } else {
       int jj = j - 1, grp = jj / NI;
       k = jj - grp * NI;
       kind = grp < 2 ? 1 : 2;
       F = grp & 1;
-      if (!((q.want >> F) & 1)) continue;
-      if (seg && (sblock || blocked[F])) continue;
-      if (kind == 2 && !S.inst[k].moved) continue;
-      if (kind == 2 && !seg && best_leaf[F] < 0) continue;  // escaped ray: no edge, no crossings
+      if (!((q.want >> F) & 1)) RR_SKIP_JOB
+      else if (seg && (sblock || blocked[F])) RR_SKIP_JOB
+      else if (kind == 2 && (!S.inst[k].moved || (q.want & QW_NO_CROSS))) RR_SKIP_JOB
+      else if (kind == 2 && !seg && best_leaf[F] < 0) RR_SKIP_JOB  // escaped ray: no edge, no crossings
     }
+    if (mine) {
     int root, place = 0;
     float tmin = S.eps, tmax;
     float3 o = q.o, d = q.d;
@@ -209,11 +283,11 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
       place = kind == 1 ? F : 1 - F;
       tmax = kind == 1 ? best_t[F] : (seg ? L - S.eps : best_t[F] - S.eps);
       float3 inv = rcp3(d);
-      if (!inst_box(I, place, o, inv, tmin, tmax)) continue;
+      if (!inst_box(I, place, o, inv, tmin, tmax)) RR_SKIP_JOB
       o = xf_point(I.Mi[place], q.o);
       d = xf_vec(I.Mi[place], q.d);
       root = I.root;
-      if (kind == 2) {
+      if (mine && kind == 2) {
         qc.inst++;
         if (seen_state != F) {
           ns = 0;
@@ -221,9 +295,13 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
         }
       }
     }
+    if (mine) {
     const float Lc = seg ? L : best_t[F];  // segment length for the (L - t) crossing sums
     WRay wr = make_wray(o, d);
-    traverse<COUNT>(S, root, wr, tmin, tmax, [&](int li, float t, float tm, int id) -> float {
+#if RR_COUNT_JOBS
+    const uint32_t nodes0 = COUNT ? qc.tc.nodes : 0;
+#endif
+    traverse<COUNT, SYNC>(S, root, wr, tmin, tmax, [&](int li, float t, float tm, int id) -> float {
       if (kind == 2) {  // ghost crossing (all hits, dedup within dedup_tol)
         if (fabsf(t - q.seed_t) < S.dedup_tol || (id == q.seed_tri && q.seed_t > 0.0f)) return tm;  // x_G: added exactly
         for (int a = 0; a < ns; ++a)
@@ -263,7 +341,17 @@ __device__ __forceinline__ void run_query(const DevScene& S, const Query& q, QRe
       }
       return t;
     }, qc.tc);
+#if RR_COUNT_JOBS
+    if (COUNT && kind != 0) {
+      qc.tc.inst_nodes += qc.tc.nodes - nodes0;
+      if (kind == 2) qc.tc.ghost_nodes += qc.tc.nodes - nodes0;
+    }
+#endif
+    }  // mine (after the instance-box test)
+    }  // mine
+    if (SYNC) __syncwarp(grp_mask);
   }
+#undef RR_SKIP_JOB
   for (int F = 0; F < 2; ++F) {
     if (!((q.want >> F) & 1)) continue;
     if (seg) {

@@ -668,8 +668,9 @@ __device__ void bidir_start_issue(const DevScene& S, const KArgs& A, int tech, i
     G.start = xg;
     G.dir0 = dir;
     G.dir1 = dir * -1.0f;
-    G.q0 = B.push(mk_ray(xg.p, dir, -1, bit(F)));
-    G.q1 = B.push(mk_ray(xg.p, G.dir1, -1, bit(F)));
+    // the start rays' own ghost crossings are not used (the edge (z_1, y_1) is queried as a whole next step)
+    G.q0 = B.push(mk_ray(xg.p, dir, -1, bit(F) | QW_NO_CROSS));
+    G.q1 = B.push(mk_ray(xg.p, G.dir1, -1, bit(F) | QW_NO_CROSS));
   }
 }
 __device__ void bidir_start_consume(const DevScene& S, int tech, int F, BPath& G, const Batch& B) {
@@ -1053,6 +1054,9 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
   o.A = &A;
   o.qc.closest = o.qc.shadow = o.qc.inst = 0;
   o.qc.tc.nodes = o.qc.tc.tris = 0;
+#if RR_COUNT_JOBS
+  if (COUNT) o.qc.tc.inst_nodes = o.qc.tc.ghost_nodes = 0;
+#endif
   o.conns = o.acc = o.rej = o.unp = o.monly = o.recon = o.splats = o.offscreen = o.zero = 0;
   for (int r = 0; r < 6; ++r) o.rejby[r] = 0;
   uint32_t nsamp = 0;
@@ -1111,9 +1115,9 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
     sc[4] += active;
     for (int k = 0; k < nmax; ++k)
 #if RR_VAR_KERNELS
-      if (k < B.n) run_query<COUNT>(S, B.q[k], B.r[k], o.qc, A.t6_centroid, A.n_centroid);
+      if (k < B.n) run_query<COUNT, false>(S, B.q[k], B.r[k], o.qc, A.t6_centroid, A.n_centroid);
 #else
-      if (k < B.n) run_query<COUNT>(S, B.q[k], B.r[k], o.qc);
+      if (k < B.n) run_query<COUNT, false>(S, B.q[k], B.r[k], o.qc);
 #endif
     if (active) {
       sc[2]++;
@@ -1143,6 +1147,12 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
   for (int r = 0; r < 6; ++r) warp_add(stt + STAT_REJBY + r, o.rejby[r]);
   for (int r = 0; r < 5; ++r)
     if (sc[r]) atomicAdd(stt + STAT_SCHED + r, sc[r]);
+#if RR_COUNT_JOBS
+  if (COUNT) {  // sched[6] / [7]: nodes fetched in dynamic-instance jobs / in ghost-crossing jobs
+    warp_add(stt + STAT_SCHED + 6, o.qc.tc.inst_nodes);
+    warp_add(stt + STAT_SCHED + 7, o.qc.tc.ghost_nodes);
+  }
+#endif
 }
 
 template <bool COUNT>
@@ -1215,7 +1225,7 @@ __global__ void k_trace(const __grid_constant__ DevScene S, int F, uint32_t n, c
   if (t >= n) return;
   QCount qc = {};
   QRes res;
-  run_query<true>(S, trace_query(rays + 8 * t, F), res, qc);
+  run_query<true, true>(S, trace_query(rays + 8 * t, F), res, qc);
   trace_store(S, F, rays + 8 * t, res, hits + 8 * t);
 }
 
@@ -1225,7 +1235,7 @@ __global__ void k_segment(const __grid_constant__ DevScene S, uint32_t n, const 
   const float* s = segs + 6 * t;
   QCount qc = {};
   QRes r;
-  run_query<true>(S, mk_seg(p3(f3(s[0], s[1], s[2])), p3(f3(s[3], s[4], s[5])), -1, -1, 3), r, qc);
+  run_query<true, true>(S, mk_seg(p3(f3(s[0], s[1], s[2])), p3(f3(s[3], s[4], s[5])), -1, -1, 3), r, qc);
   float* o = out + 10 * t;
   for (int F = 0; F < 2; ++F) {
     o[5 * F] = r.ok[F] ? 1.0f : 0.0f;
