@@ -19,6 +19,12 @@
 #include "rr_device.cuh"
 #include "rr_internal.h"
 #include "rr_kernels.h"
+#ifndef RR_SAMPLE_SORT
+#define RR_SAMPLE_SORT 1  // T3 / T6 samples processed in start-ray order (sample_order); 0: index order
+#endif
+#ifndef RR_SORT_MASK
+#define RR_SORT_MASK 0x7Fu  // techniques sorted (bit l-1): all (T7 by 2D Morton order of its pixel)
+#endif
 
 using namespace rr;
 
@@ -53,6 +59,9 @@ struct rr_ctx {
   DevBuf<float4> emit_centroid;      // RR_T6_TOWARD_LIGHT: area-weighted centroid of each emitter (world, set_edit)
   std::vector<std::vector<uint32_t>> emit_tris_host;
   DevBuf<unsigned long long> stats, work;
+  // T3 / T6 processing order (sample_order): sort keys / slots, sorted keys, permutation, CUB scratch (grow-only)
+  DevBuf<uint32_t> ord_keys, ord_vals, ord_keys2, ord_perm;
+  DevBuf<unsigned char> ord_tmp;
   DevScene S;
   uint32_t last_mask = 0;
   int edited_equals_moved = 0;
@@ -806,6 +815,7 @@ static KArgs make_kargs(rr_ctx* c, const rr_render_args* a, uint32_t mask, int l
   uint64_t local_blocks = nb > a->shard_index ? (nb - a->shard_index + a->shard_count - 1) / a->shard_count : 0;
   K.n_local = local_blocks << 16;
   K.stats = c->stats.p;
+  K.perm = nullptr;
   return K;
 }
 // grid of one residual launch (persistent lanes, rr_residual.cu)
@@ -842,6 +852,44 @@ rr_status rr_render_residual(rr_ctx* c, const rr_render_args* a, float* d_image,
       K.image = d_image;
       K.work = c->work.p + (nl++);
       if (K.n_local == 0) continue;
+#if RR_SAMPLE_SORT
+      const bool sortable = (l <= 3 && c->S.n_edited > 0) || (l >= 4 && l <= 6 && c->S.n_moved > 0) ||
+                            (l == 7 && c->cam.width <= 16384 && c->cam.height <= 8192);
+      // start-ray order (sample_order); small launches keep index order (the sort's two extra launches cost more)
+      if (((RR_SORT_MASK >> (l - 1)) & 1u) && sortable && K.n_local >= (1ull << 18)) {
+        try {
+          const size_t n = (size_t)K.n_local;
+          // box of the start points: the dynamic (edited) objects in state `side` for T1-T3, the moved objects at
+          // the other state's placement (the base path's ghosts) for T4-T6
+          float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
+          const int place = l <= 3 ? side : 1 - side;
+          for (int k = 0; k < c->S.n_inst; ++k) {
+            const DevInstance& I = c->S.inst[k];
+            if (l >= 4 && !I.moved) continue;
+            for (int q = 0; q < 3; ++q) {
+              lo[q] = std::min(lo[q], I.lo[place][q]);
+              hi[q] = std::max(hi[q], I.hi[place][q]);
+            }
+          }
+          const size_t need = sample_order(c->S, K, lo, hi, nullptr, nullptr, nullptr, nullptr, nullptr, 0, st);
+          if (c->ord_perm.cap < n) {
+            for (DevBuf<uint32_t>* b : {&c->ord_keys, &c->ord_vals, &c->ord_keys2, &c->ord_perm}) {
+              b->alloc(n);
+              b->cap = n;
+            }
+          }
+          if (c->ord_tmp.cap < need) {
+            c->ord_tmp.alloc(need);
+            c->ord_tmp.cap = need;
+          }
+          sample_order(c->S, K, lo, hi, c->ord_keys.p, c->ord_vals.p, c->ord_keys2.p, c->ord_perm.p, c->ord_tmp.p,
+                       c->ord_tmp.cap, st);
+          K.perm = c->ord_perm.p;
+        } catch (std::bad_alloc&) {
+          K.perm = nullptr;  // no scratch: index order (same image)
+        }
+      }
+#endif
       launch_residual(c->S, K, prepare_launch(c, K), st);
       if (ne < 16) cudaEventRecord(c->ev[ne++], st);
     }

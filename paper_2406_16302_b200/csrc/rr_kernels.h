@@ -37,6 +37,7 @@ struct KArgs {
   int tobj;                          // RR_TOBJ_MIDPATH (variants instantiation)
   int recon_bidir;                   // RR_RECONNECT_BIDIR (variants instantiation)
   uint64_t i_begin;
+  const uint32_t* perm;              // T3 / T6: processing order of the local slots (sample_order), else null
   rr_path_record* recs;
   unsigned long long* rec_count;
   uint64_t rec_cap;
@@ -49,6 +50,12 @@ int residual_grid(bool bidir, uint64_t n);  // blocks of residual_block() thread
 int residual_block();
 void launch_primal(const DevScene& S, int F, uint64_t seed, int D, uint32_t spp, float* image,
                    unsigned long long* stats, bool count, bool shared_streams, cudaStream_t st);
+// Processing order of T1-T6: the local sample slots sorted by the start ray of their base path (Morton code of the
+// start point, then direction bin), so that a warp's lanes trace neighbouring rays.  Returns the bytes of
+// scratch needed when keys == nullptr.  Order only: every sample is still rendered once (rr_residual.cu).
+// lo / hi: world box of the start points (the technique's sample set in the base path's state).
+size_t sample_order(const DevScene& S, const KArgs& A, const float lo[3], const float hi[3], uint32_t* keys,
+                    uint32_t* vals, uint32_t* keys2, uint32_t* perm, void* tmp, size_t tmp_bytes, cudaStream_t st);
 void launch_philox(uint32_t n, const uint32_t* ctr, uint32_t k0, uint32_t k1, uint32_t* out, cudaStream_t st);
 void launch_trace(const DevScene& S, int F, uint32_t n, const float* rays, float* hits, cudaStream_t st);
 void launch_segment(const DevScene& S, uint32_t n, const float* segs, float* out, cudaStream_t st);

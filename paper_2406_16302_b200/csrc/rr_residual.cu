@@ -24,6 +24,9 @@
 
 #include <algorithm>
 #include <mutex>
+#if !RR_VNDF_KERNELS && !RR_VAR_KERNELS
+#include <cub/device/device_radix_sort.cuh>  // sample_order (T3 / T6 processing order)
+#endif
 
 #include "rr_device.cuh"
 #include "rr_kernels.h"
@@ -1082,6 +1085,7 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
           if (A.dump) {
             i = A.i_begin + li;
           } else {
+            if (A.perm) li = __ldg(A.perm + li);  // T3 / T6: start-ray order (sample_order)
             uint64_t blk = li >> 16, off = li & 0xFFFFull;
             i = ((blk * A.shard_count + A.shard_index) << 16) | off;
             valid = i < A.n_total;
@@ -1244,6 +1248,133 @@ __global__ void k_segment(const __grid_constant__ DevScene S, uint32_t n, const 
     o[5 * F + 3] = r.c[F].sa;
     o[5 * F + 4] = r.c[F].sb;
   }
+}
+
+// ---- processing order (sample_order): sort key of the base path's start ray
+#ifndef RR_SORT_KEY
+#define RR_SORT_KEY 2  // 0: direction major, 1: position major (7 bits per axis), 2: finer directions, 3: position major (8 bits)
+#endif
+#if RR_SORT_KEY == 3
+#define RR_SORT_BITS 31
+#else
+#define RR_SORT_BITS 28
+#endif
+__device__ __forceinline__ uint32_t spread7(uint32_t v) {  // 7 bits -> every third bit
+  v &= 0x7Fu;
+  v = (v | (v << 8)) & 0x0300F00Fu;
+  v = (v | (v << 4)) & 0x030C30C3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+__device__ __forceinline__ uint32_t spread2(uint32_t v) {  // 14 bits -> every second bit
+  v &= 0x3FFFu;
+  v = (v | (v << 8)) & 0x00FF00FFu;
+  v = (v | (v << 4)) & 0x0F0F0F0Fu;
+  v = (v | (v << 2)) & 0x33333333u;
+  v = (v | (v << 1)) & 0x55555555u;
+  return v;
+}
+__global__ void k_sample_keys(const __grid_constant__ DevScene S, const __grid_constant__ KArgs A, float3 blo,
+                              float3 bsc, uint32_t* keys, uint32_t* vals) {
+  for (uint64_t li = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; li < A.n_local;
+       li += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t blk = li >> 16, off = li & 0xFFFFull;
+    const uint64_t i = ((blk * A.shard_count + A.shard_index) << 16) | off;
+    uint32_t key = (1u << RR_SORT_BITS) - 1u;
+    if (i < A.n_total) {
+      Rng rng;
+      rng.i_lo = (uint32_t)i;
+      rng.i_hi = (uint32_t)(i >> 32);
+      rng.ls = (uint32_t)A.tech | ((uint32_t)A.side << 8);
+      rng.k0 = (uint32_t)A.seed;
+      rng.k1 = (uint32_t)(A.seed >> 32);
+      float d0[8];
+      rng.dims(0, d0);
+      if (A.tech == 7) {  // camera rays: pixels in 2D Morton order (the samples of a pixel stay in index order)
+        const uint32_t npix = (uint32_t)(S.W * S.H), pix = (uint32_t)(i % npix);
+        key = spread2(pix % (uint32_t)S.W) | (spread2(pix / (uint32_t)S.W) << 1);
+        keys[li] = key;
+        vals[li] = (uint32_t)li;
+        continue;
+      }
+      P3 x;
+      float3 dir = f3(0.0f, 0.0f, 1.0f);
+      if (A.tech == 6) {  // x_G and the uniform-sphere direction (bidir_start_issue)
+        x = sample_set(S, S.moved_tris, S.moved_cdf, S.n_moved, 1 - A.side, d0[0], d0[1], d0[2]).p;
+        const float z = 1.0f - 2.0f * d0[3], rr = 2.0f * sqrtf(d0[3] * (1.0f - d0[3]));
+        float sn, cs;
+        sincosf(2.0f * RR_PI_F * d0[4], &sn, &cs);
+        dir = f3(rr * cs, rr * sn, z);
+      } else if (A.tech == 3) {  // x_D and its cosine-distributed emitter-side direction
+        const PV xd = sample_set(S, S.edited_tris, S.edited_cdf, S.n_edited, A.side, d0[0], d0[1], d0[2]);
+        x = xd.p;
+        const float r = sqrtf(d0[3]);
+        float sn, cs;
+        sincosf(2.0f * RR_PI_F * d0[4], &sn, &cs);
+        dir = to_world(xd.n, r * cs, r * sn, sqrtf(fmaxf(0.0f, 1.0f - d0[3])));
+      } else if (A.tech == 4 || A.tech == 5) {  // x_G (start_issue): the start ray's far end
+        x = sample_set(S, S.moved_tris, S.moved_cdf, S.n_moved, 1 - A.side, d0[0], d0[1], d0[2]).p;
+      } else {  // T1 / T2: x_D
+        x = sample_set(S, S.edited_tris, S.edited_cdf, S.n_edited, A.side, d0[0], d0[1], d0[2]).p;
+      }
+      // the start point in the box of its sample set (blo, 1 / extent = bsc), [0, 1) per axis
+      const float3 q = f3((float)(x.x - blo.x) * bsc.x, (float)(x.y - blo.y) * bsc.y, (float)(x.z - blo.z) * bsc.z);
+#if RR_SORT_KEY == 2
+      // finer direction bins (5 bits of z, 5 of the azimuth), 6 bits per axis of the start point
+      const uint32_t zb = min(31u, (uint32_t)((1.0f - dir.z) * 16.0f));
+      const uint32_t pb = min(31u, (uint32_t)((atan2f(dir.y, dir.x) + RR_PI_F) * (32.0f / (2.0f * RR_PI_F))));
+      const uint32_t mx = (uint32_t)fminf(fmaxf(q.x * 64.0f, 0.0f), 63.0f);
+      const uint32_t my = (uint32_t)fminf(fmaxf(q.y * 64.0f, 0.0f), 63.0f);
+      const uint32_t mz = (uint32_t)fminf(fmaxf(q.z * 64.0f, 0.0f), 63.0f);
+      key = ((zb << 5 | pb) << 18) | (spread7(mx) << 2) | (spread7(my) << 1) | spread7(mz);
+#else
+      // direction bin (3 bits of z, 4 bits of the azimuth) and the start point's Morton code in a cube of 2 diag
+      // about the camera (7 bits per axis); RR_SORT_KEY 0: direction major, 1: position major
+      const uint32_t zb = min(7u, (uint32_t)((1.0f - dir.z) * 4.0f));
+      const uint32_t pb = min(15u, (uint32_t)((atan2f(dir.y, dir.x) + RR_PI_F) * (16.0f / (2.0f * RR_PI_F))));
+      const uint32_t mx = (uint32_t)fminf(fmaxf(q.x * 128.0f, 0.0f), 127.0f);
+      const uint32_t my = (uint32_t)fminf(fmaxf(q.y * 128.0f, 0.0f), 127.0f);
+      const uint32_t mz = (uint32_t)fminf(fmaxf(q.z * 128.0f, 0.0f), 127.0f);
+      const uint32_t mort = (spread7(mx) << 2) | (spread7(my) << 1) | spread7(mz);
+#if RR_SORT_KEY == 1
+      key = (mort << 7) | (zb << 4 | pb);
+#elif RR_SORT_KEY == 3
+      {  // position major with 8 bits per axis
+        const uint32_t ax = (uint32_t)fminf(fmaxf(q.x * 256.0f, 0.0f), 255.0f);
+        const uint32_t ay = (uint32_t)fminf(fmaxf(q.y * 256.0f, 0.0f), 255.0f);
+        const uint32_t az = (uint32_t)fminf(fmaxf(q.z * 256.0f, 0.0f), 255.0f);
+        const uint32_t m8 = (spread7(ax >> 1) << 5) | (spread7(ay >> 1) << 4) | (spread7(az >> 1) << 3) |
+                            ((ax & 1u) << 2) | ((ay & 1u) << 1) | (az & 1u);
+        key = (m8 << 7) | (zb << 4 | pb);
+      }
+#else
+      key = ((zb << 4 | pb) << 21) | mort;
+#endif
+#endif
+    }
+    keys[li] = key;
+    vals[li] = (uint32_t)li;
+  }
+}
+size_t sample_order(const DevScene& S, const KArgs& A, const float lo[3], const float hi[3], uint32_t* keys,
+                    uint32_t* vals, uint32_t* keys2, uint32_t* perm, void* tmp, size_t tmp_bytes, cudaStream_t st) {
+  const int n = (int)A.n_local;
+  if (!keys) {
+    size_t need = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, need, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, n, 0, RR_SORT_BITS, st);
+    return need;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  float3 blo = f3(lo[0], lo[1], lo[2]), bsc;
+  bsc.x = 1.0f / fmaxf(hi[0] - lo[0], 1e-20f);
+  bsc.y = 1.0f / fmaxf(hi[1] - lo[1], 1e-20f);
+  bsc.z = 1.0f / fmaxf(hi[2] - lo[2], 1e-20f);
+  k_sample_keys<<<sms * 8, 256, 0, st>>>(S, A, blo, bsc, keys, vals);
+  cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, perm, n, 0, RR_SORT_BITS, st);
+  return 0;
 }
 
 // ---- host launchers
