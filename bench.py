@@ -309,6 +309,7 @@ def run_ours(a):
     tm = r.last_timings(16)
     launch_ms = [x for x in tm[1:15] if x > 0]
     launches = len(launch_ms)
+    sorted_launches = int(r.get_stats()["sched"][1])  # launches with the sample-ordering pre-pass (key kernel + sort)
     kern_ms = sum(launch_ms)
     for k in stats_acc:
         stats_acc[k] = st[k]
@@ -423,7 +424,11 @@ def run_ours(a):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches * a.steps,
+            # residual kernels + our sample-key kernels; each key kernel is followed by one CUB radix sort
+            # (library kernels, not counted here); ordering pre-passes take ordering_ms_per_step of the step
+            "gpu_launches": (launches + sorted_launches) * a.steps,
+            "cub_radix_sorts_per_step": sorted_launches,
+            "ordering_ms_per_step": float(tm[15]),
             "clocks": clk,
             "upload_s": upload_s,
         }

@@ -174,8 +174,8 @@ typedef struct {
                               a sample summed over rounds, [5] deepest BVH root-to-leaf path in inner
                               nodes (scene property; upload fails above RR_STACK = 64), [6] / [7] internal nodes fetched
                               in dynamic-instance / ghost-crossing BLAS jobs (RR_COUNT_TRAVERSAL in a library built with
-                              -DRR_COUNT_JOBS=1, tools/variants.py; else 0), ([1]
-                              reserved, 0) */
+                              -DRR_COUNT_JOBS=1, tools/variants.py; else 0), [1] residual launches that
+                              had the sample-ordering pre-pass (one key kernel + one CUB radix sort each) */
   uint64_t r_hist[16];     /* accepted connections of reconnected pairs (R != 1, C7) by floor(log2 R) + 8, clamped to
                               [0, 15]: bin b holds R in [2^(b-8), 2^(b-7)) (SURVEY 8(f) row 3, R statistics) */
 } rr_stats;
@@ -254,7 +254,8 @@ rr_status rr_dump_paths(rr_ctx* ctx, const rr_render_args* args, uint32_t techni
                         uint64_t i_begin, uint64_t i_end, rr_path_record* host_out, uint64_t capacity,
                         uint64_t* n_out);
 /* Timing of the last render's kernels, in ms (events on the render stream): out[0] = total,
- * out[1..14] = per (technique, side) launch.  Blocking. */
+ * out[1..14] = per (technique, side) residual kernel (its own launch only), out[15] = the rest of the render
+ * (image / counter clears and the sample-ordering pre-passes).  Blocking. */
 rr_status rr_last_timings(rr_ctx* ctx, float* out, uint32_t n);
 
 #ifdef __cplusplus

@@ -67,7 +67,8 @@ struct rr_ctx {
   int edited_equals_moved = 0;
   std::vector<uint32_t> flags_host;
   // timings
-  cudaEvent_t ev[16];
+  cudaEvent_t ev[32];  // render start, then (start, end) of each residual launch
+  int n_sorted = 0;     // residual launches of the last render that had the sample-ordering pre-pass
   int n_ev = 0;
   bool ev_init = false;
 };
@@ -157,7 +158,7 @@ void rr_destroy(rr_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->ev_init)
-    for (int k = 0; k < 16; ++k) cudaEventDestroy(c->ev[k]);
+    for (int k = 0; k < 32; ++k) cudaEventDestroy(c->ev[k]);
   delete c;
 }
 
@@ -832,7 +833,7 @@ rr_status rr_render_residual(rr_ctx* c, const rr_render_args* a, float* d_image,
   if (cuda_check(c, "before render") != RR_OK) return RR_E_CUDA;
   cudaStream_t st = (cudaStream_t)stream;
   if (!c->ev_init) {
-    for (int k = 0; k < 16; ++k) cudaEventCreate(&c->ev[k]);
+    for (int k = 0; k < 32; ++k) cudaEventCreate(&c->ev[k]);
     c->ev_init = true;
   }
   uint32_t mask = eff_mask(c, a->technique_mask);
@@ -842,6 +843,7 @@ rr_status rr_render_residual(rr_ctx* c, const rr_render_args* a, float* d_image,
   cudaMemsetAsync(c->stats.p, 0, STAT_COUNT * sizeof(unsigned long long), st);
   cudaMemsetAsync(c->work.p, 0, 16 * sizeof(unsigned long long), st);
   int ne = 0, nl = 0;
+  c->n_sorted = 0;
   cudaEventRecord(c->ev[ne++], st);
   int sides = (a->flags & RR_TWO_WAY) ? 2 : 1;
   for (int l = 1; l <= 7; ++l) {
@@ -885,13 +887,15 @@ rr_status rr_render_residual(rr_ctx* c, const rr_render_args* a, float* d_image,
           sample_order(c->S, K, lo, hi, c->ord_keys.p, c->ord_vals.p, c->ord_keys2.p, c->ord_perm.p, c->ord_tmp.p,
                        c->ord_tmp.cap, st);
           K.perm = c->ord_perm.p;
+          c->n_sorted++;
         } catch (std::bad_alloc&) {
           K.perm = nullptr;  // no scratch: index order (same image)
         }
       }
 #endif
+      if (ne < 31) cudaEventRecord(c->ev[ne++], st);
       launch_residual(c->S, K, prepare_launch(c, K), st);
-      if (ne < 16) cudaEventRecord(c->ev[ne++], st);
+      if (ne < 32) cudaEventRecord(c->ev[ne++], st);
     }
   }
   c->n_ev = ne;
@@ -960,6 +964,7 @@ rr_status rr_get_stats(rr_ctx* c, rr_stats* out) {
   for (int r = 0; r < 8; ++r) out->sched[r] = h[STAT_SCHED + r];
   for (int r = 0; r < 16; ++r) out->r_hist[r] = h[STAT_RHIST + r];
   out->sched[5] = (uint64_t)c->bvh_depth;
+  out->sched[1] = (uint64_t)c->n_sorted;
   out->effective_mask = c->last_mask;
   out->n_moved = 0;
   for (int k = 0; k < c->S.n_inst; ++k) out->n_moved += c->S.inst[k].moved ? 1 : 0;
@@ -970,10 +975,17 @@ rr_status rr_last_timings(rr_ctx* c, float* out, uint32_t n) {
   if (!c || !out) return RR_E_INVALID;
   cudaSetDevice(c->device);
   for (uint32_t k = 0; k < n; ++k) out[k] = 0.0f;
-  if (c->n_ev < 2) return RR_OK;
+  if (c->n_ev < 3) return RR_OK;
   cudaEventSynchronize(c->ev[c->n_ev - 1]);
   if (n > 0) cudaEventElapsedTime(&out[0], c->ev[0], c->ev[c->n_ev - 1]);
-  for (int k = 1; k < c->n_ev && (uint32_t)k < n; ++k) cudaEventElapsedTime(&out[k], c->ev[k - 1], c->ev[k]);
+  float kern = 0.0f;
+  for (int k = 1; 2 * k < c->n_ev; ++k) {  // launch k: events 2k-1 (start) and 2k (end)
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, c->ev[2 * k - 1], c->ev[2 * k]);
+    kern += ms;
+    if ((uint32_t)k < n && k < 15) out[k] = ms;
+  }
+  if (n > 15) out[15] = out[0] - kern;  // outside the residual kernels: clears and the ordering pre-passes
   return cuda_check(c, "timings");
 }
 
