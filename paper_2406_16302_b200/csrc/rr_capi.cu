@@ -22,6 +22,9 @@
 #ifndef RR_SAMPLE_SORT
 #define RR_SAMPLE_SORT 1  // T3 / T6 samples processed in start-ray order (sample_order); 0: index order
 #endif
+#ifndef RR_REFILL
+#define RR_REFILL 32  // lanes of a warp refilled together (1: immediate per-lane refill)
+#endif
 #ifndef RR_SORT_MASK
 #define RR_SORT_MASK 0x7Fu  // techniques sorted (bit l-1): all (T7 by 2D Morton order of its pixel)
 #endif
@@ -817,6 +820,11 @@ static KArgs make_kargs(rr_ctx* c, const rr_render_args* a, uint32_t mask, int l
   K.n_local = local_blocks << 16;
   K.stats = c->stats.p;
   K.perm = nullptr;
+  // batch refill (rr_residual.cu residual_loop): a warp's free lanes take new samples together once RR_REFILL lanes
+  // are free, so the lanes of a batch start from neighbouring (ordered) samples and advance in step; T1 / T4 (short,
+  // emitter-rooted samples of very different lengths) with half warps (config 4: 4.93 s at 32 for every technique
+  // vs 7.01 s with immediate refill; T1 / T4 alone were faster at 8-16)
+  K.refill_min = (l == 1 || l == 4) ? RR_REFILL / 2 : RR_REFILL;
   return K;
 }
 // grid of one residual launch (persistent lanes, rr_residual.cu)

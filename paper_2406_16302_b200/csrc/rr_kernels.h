@@ -37,7 +37,8 @@ struct KArgs {
   int tobj;                          // RR_TOBJ_MIDPATH (variants instantiation)
   int recon_bidir;                   // RR_RECONNECT_BIDIR (variants instantiation)
   uint64_t i_begin;
-  const uint32_t* perm;              // T3 / T6: processing order of the local slots (sample_order), else null
+  const uint32_t* perm;              // processing order of the local slots (sample_order), else null
+  int refill_min;                    // free lanes of a warp that take new samples together (1: each at once)
   rr_path_record* recs;
   unsigned long long* rec_count;
   uint64_t rec_cap;

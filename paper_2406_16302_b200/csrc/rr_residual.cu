@@ -1051,6 +1051,9 @@ __device__ __forceinline__ uint64_t fetch_work(unsigned long long* counter, bool
                           // latency hiding beats the spills)
 #endif
 
+#ifndef RR_MEGA_SYNC
+#define RR_MEGA_SYNC false  // traversal with a ballot per iteration in the megakernels (rr_query.cuh traverse)
+#endif
 template <class State, bool BIDIR, bool COUNT>
 __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A) {
   Out o;
@@ -1074,7 +1077,11 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
     if (!active) B.n = 0;
     while (true) {
       bool need = !active && more;
-      if (!__any_sync(FULLMASK, need)) break;
+      const unsigned nm = __ballot_sync(FULLMASK, need);
+      if (!nm) break;
+      // batch refill: free lanes wait until A.refill_min lanes are free (or none is busy), then take consecutive
+      // (ordered, hence neighbouring) samples together, so the warp's lanes start and advance in step
+      if (__popc(nm) < A.refill_min && __any_sync(FULLMASK, active)) break;
       uint64_t li = fetch_work(A.work, need);
       if (need) {
         if (li >= A.n_local) {
@@ -1119,9 +1126,9 @@ __device__ __forceinline__ void residual_loop(const DevScene& S, const KArgs& A)
     sc[4] += active;
     for (int k = 0; k < nmax; ++k)
 #if RR_VAR_KERNELS
-      if (k < B.n) run_query<COUNT, false>(S, B.q[k], B.r[k], o.qc, A.t6_centroid, A.n_centroid);
+      if (k < B.n) run_query<COUNT, RR_MEGA_SYNC>(S, B.q[k], B.r[k], o.qc, A.t6_centroid, A.n_centroid);
 #else
-      if (k < B.n) run_query<COUNT, false>(S, B.q[k], B.r[k], o.qc);
+      if (k < B.n) run_query<COUNT, RR_MEGA_SYNC>(S, B.q[k], B.r[k], o.qc);
 #endif
     if (active) {
       sc[2]++;
