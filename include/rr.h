@@ -217,7 +217,11 @@ rr_status rr_set_edit(rr_ctx* ctx, uint32_t n, const rr_edit* edits);
 
 /* Render this shard's residual estimate into d_image_rgba (H*W*4 fp32, device, channel 3 = 0), the
  * final normalised estimate: the sum over all shards is the full estimate of I_new - I_old.
- * Asynchronous on cuda_stream.  Errors: RR_E_INVALID, RR_E_STATE, RR_E_CUDA, RR_E_OOM. */
+ * Asynchronous on cuda_stream: the call only enqueues work there (memsets, the sample-ordering pre-pass, one
+ * kernel per (technique, side)) and never synchronises, so after one warm-up render with the same arguments
+ * (which grows the context's scratch buffers) it may run under CUDA stream capture and be replayed as a graph;
+ * rr_last_timings is then meaningless until the next direct render.
+ * Errors: RR_E_INVALID, RR_E_STATE, RR_E_CUDA, RR_E_OOM. */
 rr_status rr_render_residual(rr_ctx* ctx, const rr_render_args* args, float* d_image_rgba, uint64_t cuda_stream);
 
 /* Same as rr_render_residual but with HOST image memory (h_image_rgba, H*W*4 fp32): the library copies

@@ -5,6 +5,8 @@
 // Replaces the paper's Embree BVH.
 #include <cub/cub.cuh>
 
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "rr_device.cuh"
@@ -244,6 +246,147 @@ __global__ void k_pack(const float4* __restrict__ tris, const uint32_t* __restri
   nd[3] = make_float4(__int_as_float(e0), __int_as_float(e1), 0.0f, 0.0f);
 }
 
+#ifndef RR_ROTATE
+#define RR_ROTATE 0  // bottom-up tree-rotation passes over the packed nodes after the LBVH build (k_rotate)
+#endif
+// ------------------------------------------------------------------------------------------------
+// Tree rotations (Kensler 2008 "Tree rotations for improving bounding volume hierarchies"), bottom-up over the
+// packed BVH2 nodes with the refit's arrival counters: the second thread to reach a node N = (A, B) finds both
+// subtrees final, and may swap a child with a grandchild on the other side (B <-> A0 / A1, A <-> B0 / B1) or two
+// grandchildren (A0 <-> B0 / B1) when that shrinks the surface area of the re-formed child box(es).  Only N and
+// its children are rewritten; N's own box (held by its parent) is the union of the same leaves and does not
+// change.  A rotation is taken only if the height of N's subtree does not grow, so the tree never gets deeper
+// than the LBVH it started from (the traversal-stack bound checked at upload still holds).  Not an SAH build:
+// the topology stays the radix tree's up to these local swaps.
+struct PNode {
+  Box b[2];
+  int e[2];
+};
+__device__ __forceinline__ PNode load_pnode_cg(const float4* nodes, int idx) {
+  const float4 a = __ldcg(nodes + 4 * idx), b = __ldcg(nodes + 4 * idx + 1), c = __ldcg(nodes + 4 * idx + 2),
+               d = __ldcg(nodes + 4 * idx + 3);
+  PNode n;
+  n.b[0].lo[0] = a.x; n.b[0].hi[0] = a.y; n.b[0].lo[1] = a.z; n.b[0].hi[1] = a.w; n.b[0].lo[2] = c.x; n.b[0].hi[2] = c.y;
+  n.b[1].lo[0] = b.x; n.b[1].hi[0] = b.y; n.b[1].lo[1] = b.z; n.b[1].hi[1] = b.w; n.b[1].lo[2] = c.z; n.b[1].hi[2] = c.w;
+  n.e[0] = __float_as_int(d.x);
+  n.e[1] = __float_as_int(d.y);
+  return n;
+}
+__device__ __forceinline__ void store_pnode(float4* nodes, int idx, const PNode& n) {
+  float4* nd = nodes + 4 * idx;
+  nd[0] = make_float4(n.b[0].lo[0], n.b[0].hi[0], n.b[0].lo[1], n.b[0].hi[1]);
+  nd[1] = make_float4(n.b[1].lo[0], n.b[1].hi[0], n.b[1].lo[1], n.b[1].hi[1]);
+  nd[2] = make_float4(n.b[0].lo[2], n.b[0].hi[2], n.b[1].lo[2], n.b[1].hi[2]);
+  nd[3] = make_float4(__int_as_float(n.e[0]), __int_as_float(n.e[1]), 0.0f, 0.0f);
+}
+__device__ __forceinline__ Box box_union(const Box& a, const Box& b) {
+  Box m;
+  for (int q = 0; q < 3; ++q) {
+    m.lo[q] = fminf(a.lo[q], b.lo[q]);
+    m.hi[q] = fmaxf(a.hi[q], b.hi[q]);
+  }
+  return m;
+}
+__device__ __forceinline__ float half_area(const Box& b) {
+  const float dx = b.hi[0] - b.lo[0], dy = b.hi[1] - b.lo[1], dz = b.hi[2] - b.lo[2];
+  return dx * dy + dy * dz + dz * dx;
+}
+__global__ void k_rotate(float4* __restrict__ nodes, int n, int node_base, int leaf_base, int* __restrict__ parent_int,
+                         int* __restrict__ parent_leaf, int* __restrict__ counter, int* __restrict__ hgt,
+                         unsigned int* __restrict__ n_rot) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int p = parent_leaf[k];
+  while (p >= 0) {
+    __threadfence();
+    if (atomicAdd(&counter[p], 1) == 0) return;  // first arrival stops; the second one owns the node
+    __threadfence();
+    PNode N = load_pnode_cg(nodes, node_base + p);
+    PNode C[2];
+    int h[2], hc[2][2];
+    bool inner[2];
+    for (int s = 0; s < 2; ++s) {
+      inner[s] = N.e[s] >= 0;
+      h[s] = 0;
+      hc[s][0] = hc[s][1] = 0;
+      if (inner[s]) {
+        C[s] = load_pnode_cg(nodes, N.e[s]);
+        for (int g = 0; g < 2; ++g) hc[s][g] = C[s].e[g] < 0 ? 0 : __ldcg(hgt + (C[s].e[g] - node_base));
+        h[s] = 1 + max(hc[s][0], hc[s][1]);
+      }
+    }
+    const int h_old = 1 + max(h[0], h[1]);
+    // candidates: kind 0: child (1 - s) <-> grandchild g of inner child s;  kind 1: grandchild (0, 0) <-> (1, g)
+    float best = 0.0f;
+    int bk = -1, bs = 0, bg = 0;
+    for (int s = 0; s < 2; ++s) {
+      if (!inner[s]) continue;
+      const float base = half_area(N.b[s]);
+      for (int g = 0; g < 2; ++g) {
+        // child s re-formed from (other child, grandchild 1 - g); grandchild g moves up
+        const float d = half_area(box_union(N.b[1 - s], C[s].b[1 - g])) - base;
+        const int hs = 1 + max(h[1 - s], hc[s][1 - g]);
+        const int hn = 1 + max(hs, hc[s][g]);
+        if (d < best - 1e-4f * base && hn <= h_old) {
+          best = d;
+          bk = 0; bs = s; bg = g;
+        }
+      }
+    }
+    if (inner[0] && inner[1]) {
+      const float base = half_area(N.b[0]) + half_area(N.b[1]);
+      for (int g = 0; g < 2; ++g) {
+        // A' = (B_g, A_1), B' = (A_0, B_{1-g})
+        const float d = half_area(box_union(C[1].b[g], C[0].b[1])) + half_area(box_union(C[0].b[0], C[1].b[1 - g])) - base;
+        const int ha = 1 + max(hc[1][g], hc[0][1]), hb = 1 + max(hc[0][0], hc[1][1 - g]);
+        if (d < best - 1e-4f * base && 1 + max(ha, hb) <= h_old) {
+          best = d;
+          bk = 1; bs = 0; bg = g;
+        }
+      }
+    }
+    int h_new = h_old;
+    if (bk == 0) {
+      const int s = bs, g = bg, up = C[s].e[g], down = N.e[1 - s];
+      const int cs = N.e[s] - node_base;  // local index of the re-formed child
+      const Box upb = C[s].b[g];
+      C[s].b[g] = N.b[1 - s];
+      C[s].e[g] = down;
+      N.b[1 - s] = upb;
+      N.e[1 - s] = up;
+      N.b[s] = box_union(C[s].b[0], C[s].b[1]);
+      const int hs = 1 + max(h[1 - s], hc[s][1 - g]);
+      store_pnode(nodes, N.e[s], C[s]);
+      store_pnode(nodes, node_base + p, N);
+      hgt[cs] = hs;
+      h_new = 1 + max(hs, hc[s][g]);
+      if (down < 0) parent_leaf[~down - leaf_base] = cs; else parent_int[down - node_base] = cs;
+      if (up < 0) parent_leaf[~up - leaf_base] = p; else parent_int[up - node_base] = p;
+      atomicAdd(n_rot, 1u);
+    } else if (bk == 1) {
+      const int g = bg, x = C[0].e[0], y = C[1].e[g];
+      const int ca = N.e[0] - node_base, cb = N.e[1] - node_base;
+      const Box bx = C[0].b[0], by = C[1].b[g];
+      C[0].b[0] = by; C[0].e[0] = y;
+      C[1].b[g] = bx; C[1].e[g] = x;
+      N.b[0] = box_union(C[0].b[0], C[0].b[1]);
+      N.b[1] = box_union(C[1].b[0], C[1].b[1]);
+      store_pnode(nodes, N.e[0], C[0]);
+      store_pnode(nodes, N.e[1], C[1]);
+      store_pnode(nodes, node_base + p, N);
+      const int ha = 1 + max(hc[1][g], hc[0][1]), hb = 1 + max(hc[0][0], hc[1][1 - g]);
+      hgt[ca] = ha;
+      hgt[cb] = hb;
+      h_new = 1 + max(ha, hb);
+      if (y < 0) parent_leaf[~y - leaf_base] = ca; else parent_int[y - node_base] = ca;
+      if (x < 0) parent_leaf[~x - leaf_base] = cb; else parent_int[x - node_base] = cb;
+      atomicAdd(n_rot, 1u);
+    }
+    hgt[p] = h_new;
+    p = p == 0 ? -1 : parent_int[p];
+  }
+}
+
 // Build one BLAS over n >= 1 triangles (3 float4 each, device).  Writes max(n-1,1) nodes at node_base and n
 // leaf triangles at leaf_base.  Returns the root node index (node_base).  h_keys (optional, host, n): sort
 // keys to use instead of the triangles' own Morton codes (object-grouped keys, rr_capi.cu).
@@ -276,6 +419,22 @@ int build_lbvh(const float4* d_tris, int n, float4* d_nodes, float4* d_ltris, fl
   if (n > 1) k_karras<<<(n - 1 + TB - 1) / TB, TB, 0, st>>>(keys2.p, n, child.p, pint.p, pleaf.p);
   k_refit<<<nb, TB, 0, st>>>(d_tris, vals2.p, n, child.p, pint.p, pleaf.p, ibox.p, lbox.p, counter.p);
   k_pack<<<nb, TB, 0, st>>>(d_tris, vals2.p, n, child.p, ibox.p, lbox.p, d_nodes, d_ltris, d_lxf, node_base, leaf_base);
+  if (RR_ROTATE > 0 && n >= 3) {
+    DevBuf<int> hgt(n - 1);
+    DevBuf<unsigned int> nrot(1);
+    for (int pass = 0; pass < RR_ROTATE; ++pass) {
+      cudaMemsetAsync(counter.p, 0, sizeof(int) * (n - 1), st);
+      cudaMemsetAsync(nrot.p, 0, sizeof(unsigned int), st);
+      k_rotate<<<nb, TB, 0, st>>>(d_nodes, n, node_base, leaf_base, pint.p, pleaf.p, counter.p, hgt.p, nrot.p);
+      if (getenv("RR_ROTATE_LOG")) {  // diagnostics: rotations taken per pass
+        unsigned int r = 0;
+        cudaMemcpyAsync(&r, nrot.p, sizeof(r), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "lbvh n=%d rotate pass %d: %u rotations\n", n, pass, r);
+      }
+    }
+    cudaStreamSynchronize(st);
+  }
   cudaStreamSynchronize(st);
   return node_base;
 }

@@ -194,6 +194,9 @@ __device__ inline float3 path_value(const DevScene& S, const PV* x, const Cross*
 // ------------------------------------------------------------------------------------------------
 // splat + records + statistics
 // ------------------------------------------------------------------------------------------------
+#ifndef RR_SPLAT_MATCH
+#define RR_SPLAT_MATCH 0  // 1: warp-aggregated splat (tools/variants.py knob; measured)
+#endif
 struct Out {
   const KArgs* A;
   QCount qc;
@@ -207,6 +210,34 @@ __device__ __forceinline__ void splat(Out& o, int pix, float3 t) {
     return;
   }
   o.splats++;
+#if RR_SPLAT_MATCH
+  // warp-aggregated splat (measured and rejected): the lanes splatting in this
+  // instruction are grouped by pixel (__match_any_sync), each group's terms are summed by a rank-ordered
+  // shuffle tree and the group's lowest lane issues one atomicAdd
+  const unsigned act = __activemask();
+  const unsigned peers = __match_any_sync(act, pix);
+  if (__any_sync(act, peers & (peers - 1))) {  // some group has more than one lane
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned rank = __popc(peers & ((1u << lane) - 1u));
+    const unsigned cnt = __popc(peers);
+    for (unsigned step = 1; step < 32; step <<= 1) {
+      if (!__any_sync(act, step < cnt)) break;
+      // the lane of rank (rank + step) in my group, if any
+      unsigned above = peers >> lane >> 1;  // peers above me, bit 0 = lane + 1
+      int src = -1;
+      if ((rank & (2 * step - 1)) == 0 && rank + step < cnt) {
+        unsigned m = above;
+        for (unsigned k = 1; k < step; ++k) m &= m - 1;  // drop the (step - 1) nearest peers above
+        src = (int)lane + __ffs(m);
+      }
+      float x = __shfl_sync(act, t.x, src < 0 ? (int)lane : src);
+      float y = __shfl_sync(act, t.y, src < 0 ? (int)lane : src);
+      float z = __shfl_sync(act, t.z, src < 0 ? (int)lane : src);
+      if (src >= 0) { t.x += x; t.y += y; t.z += z; }
+    }
+    if (rank != 0) return;
+  }
+#endif
   atomicAdd(reinterpret_cast<float4*>(o.A->image) + pix, make_float4(t.x, t.y, t.z, 0.0f));
 }
 __device__ inline void emit_record(Out& o, uint64_t i, int kind, int a, int b, int status, int reason, int pix_p, float3 tp,

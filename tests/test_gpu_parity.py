@@ -552,6 +552,31 @@ def test_sharding_sums_to_unsharded(torch_cuda):
     assert float((acc - full).abs().max()) <= 1e-5 * scale
 
 
+def test_render_is_cuda_graph_capturable(torch_cuda):
+    """rr_render_residual only enqueues work on the caller's stream (include/rr.h), so after one warm-up render
+    the whole render -- ordering pre-pass and CUB sorts included (2^18 slots per launch) -- captures into a
+    CUDA graph; replays reproduce the direct render up to the order of the atomic splats."""
+    torch = torch_cuda
+    w = S.config1(64, 64, spp=64)
+    r = _renderer(w)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        img = r.render_residual(w.args)
+        s.synchronize()
+        ref = img.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        r.render_residual(w.args, image=img)
+    for _ in range(2):
+        img.fill_(7.0)
+        with torch.cuda.stream(s):
+            g.replay()
+        s.synchronize()
+        scale = float(ref.abs().max())
+        assert scale > 0 and float((img - ref).abs().max()) <= 1e-5 * scale
+    del g
+
+
 def test_invalid_arguments_are_refused(torch_cuda):
     from paper_2406_16302_b200 import RRError
     w = S.config1(16, 16)
