@@ -1,7 +1,8 @@
 // rr_lbvh.cu -- GPU LBVH build (Karras 2012 "Maximizing parallelism in the construction of BVHs,
 // octrees, and k-d trees"): 63-bit Morton codes of triangle centroids, CUB radix sort, binary radix tree
 // from longest common prefixes (duplicate keys broken by index), bottom-up AABB refit with atomic
-// arrival counters, and packing into 64-byte BVH2 nodes.  SAH-free by design (north star).
+// arrival counters, and packing into 64-byte BVH2 nodes.  The build is SAH-free (north star); RR_ROTATE passes of
+// local tree rotations (k_rotate) then shrink child boxes without deepening the tree.
 // Replaces the paper's Embree BVH.
 #include <cub/cub.cuh>
 
@@ -247,7 +248,7 @@ __global__ void k_pack(const float4* __restrict__ tris, const uint32_t* __restri
 }
 
 #ifndef RR_ROTATE
-#define RR_ROTATE 0  // bottom-up tree-rotation passes over the packed nodes after the LBVH build (k_rotate)
+#define RR_ROTATE 4  // bottom-up tree-rotation passes over the packed nodes after the LBVH build (k_rotate; 0: the plain radix tree)
 #endif
 // ------------------------------------------------------------------------------------------------
 // Tree rotations (Kensler 2008 "Tree rotations for improving bounding volume hierarchies"), bottom-up over the
