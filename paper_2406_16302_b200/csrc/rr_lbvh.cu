@@ -250,6 +250,9 @@ __global__ void k_pack(const float4* __restrict__ tris, const uint32_t* __restri
 #ifndef RR_ROTATE
 #define RR_ROTATE 4  // bottom-up tree-rotation passes over the packed nodes after the LBVH build (k_rotate; 0: the plain radix tree)
 #endif
+#ifndef RR_ROTATE_SLACK
+#define RR_ROTATE_SLACK 0  // levels by which a rotation may raise its subtree's height (0: never deeper than the radix tree)
+#endif
 // ------------------------------------------------------------------------------------------------
 // Tree rotations (Kensler 2008 "Tree rotations for improving bounding volume hierarchies"), bottom-up over the
 // packed BVH2 nodes with the refit's arrival counters: the second thread to reach a node N = (A, B) finds both
@@ -294,7 +297,7 @@ __device__ __forceinline__ float half_area(const Box& b) {
 }
 __global__ void k_rotate(float4* __restrict__ nodes, int n, int node_base, int leaf_base, int* __restrict__ parent_int,
                          int* __restrict__ parent_leaf, int* __restrict__ counter, int* __restrict__ hgt,
-                         unsigned int* __restrict__ n_rot) {
+                         unsigned int* __restrict__ n_rot, int slack) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   int p = parent_leaf[k];
@@ -317,6 +320,7 @@ __global__ void k_rotate(float4* __restrict__ nodes, int n, int node_base, int l
       }
     }
     const int h_old = 1 + max(h[0], h[1]);
+    const int h_lim = h_old + slack;  // slack 0: the subtree's height never grows
     // candidates: kind 0: child (1 - s) <-> grandchild g of inner child s;  kind 1: grandchild (0, 0) <-> (1, g)
     float best = 0.0f;
     int bk = -1, bs = 0, bg = 0;
@@ -328,7 +332,7 @@ __global__ void k_rotate(float4* __restrict__ nodes, int n, int node_base, int l
         const float d = half_area(box_union(N.b[1 - s], C[s].b[1 - g])) - base;
         const int hs = 1 + max(h[1 - s], hc[s][1 - g]);
         const int hn = 1 + max(hs, hc[s][g]);
-        if (d < best - 1e-4f * base && hn <= h_old) {
+        if (d < best - 1e-4f * base && hn <= h_lim) {
           best = d;
           bk = 0; bs = s; bg = g;
         }
@@ -340,7 +344,7 @@ __global__ void k_rotate(float4* __restrict__ nodes, int n, int node_base, int l
         // A' = (B_g, A_1), B' = (A_0, B_{1-g})
         const float d = half_area(box_union(C[1].b[g], C[0].b[1])) + half_area(box_union(C[0].b[0], C[1].b[1 - g])) - base;
         const int ha = 1 + max(hc[1][g], hc[0][1]), hb = 1 + max(hc[0][0], hc[1][1 - g]);
-        if (d < best - 1e-4f * base && 1 + max(ha, hb) <= h_old) {
+        if (d < best - 1e-4f * base && 1 + max(ha, hb) <= h_lim) {
           best = d;
           bk = 1; bs = 0; bg = g;
         }
@@ -423,18 +427,34 @@ int build_lbvh(const float4* d_tris, int n, float4* d_nodes, float4* d_ltris, fl
   if (RR_ROTATE > 0 && n >= 3) {
     DevBuf<int> hgt(n - 1);
     DevBuf<unsigned int> nrot(1);
-    for (int pass = 0; pass < RR_ROTATE; ++pass) {
-      cudaMemsetAsync(counter.p, 0, sizeof(int) * (n - 1), st);
-      cudaMemsetAsync(nrot.p, 0, sizeof(unsigned int), st);
-      k_rotate<<<nb, TB, 0, st>>>(d_nodes, n, node_base, leaf_base, pint.p, pleaf.p, counter.p, hgt.p, nrot.p);
-      if (getenv("RR_ROTATE_LOG")) {  // diagnostics: rotations taken per pass
-        unsigned int r = 0;
-        cudaMemcpyAsync(&r, nrot.p, sizeof(r), cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
-        fprintf(stderr, "lbvh n=%d rotate pass %d: %u rotations\n", n, pass, r);
+    auto rotate = [&](int slack) {
+      for (int pass = 0; pass < RR_ROTATE; ++pass) {
+        cudaMemsetAsync(counter.p, 0, sizeof(int) * (n - 1), st);
+        cudaMemsetAsync(nrot.p, 0, sizeof(unsigned int), st);
+        k_rotate<<<nb, TB, 0, st>>>(d_nodes, n, node_base, leaf_base, pint.p, pleaf.p, counter.p, hgt.p, nrot.p, slack);
+        if (getenv("RR_ROTATE_LOG")) {  // diagnostics: rotations taken per pass
+          unsigned int r = 0;
+          cudaMemcpyAsync(&r, nrot.p, sizeof(r), cudaMemcpyDeviceToHost, st);
+          cudaStreamSynchronize(st);
+          fprintf(stderr, "lbvh n=%d rotate pass %d (slack %d): %u rotations\n", n, pass, slack, r);
+        }
       }
+      int h0 = 0;  // height of the rotated tree (hgt of the root)
+      cudaMemcpyAsync(&h0, hgt.p, sizeof(int), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      return h0;
+    };
+    int h0 = rotate(RR_ROTATE_SLACK);
+    // rotations with slack may deepen the tree: if it no longer fits the traversal stack with room for an extra
+    // root above it, restore the radix tree (child / box arrays are untouched) and rotate without slack, which
+    // never deepens it
+    if (RR_ROTATE_SLACK > 0 && h0 > RR_STACK - 2) {
+      cudaMemsetAsync(pint.p, 0xff, sizeof(int) * (n - 1), st);
+      k_karras<<<(n - 1 + TB - 1) / TB, TB, 0, st>>>(keys2.p, n, child.p, pint.p, pleaf.p);
+      k_pack<<<nb, TB, 0, st>>>(d_tris, vals2.p, n, child.p, ibox.p, lbox.p, d_nodes, d_ltris, d_lxf, node_base, leaf_base);
+      h0 = rotate(0);
     }
-    cudaStreamSynchronize(st);
+    if (getenv("RR_ROTATE_LOG")) fprintf(stderr, "lbvh n=%d height after rotations %d\n", n, h0);
   }
   cudaStreamSynchronize(st);
   return node_base;
